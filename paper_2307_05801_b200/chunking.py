@@ -1,0 +1,97 @@
+"""View-chunked streaming between host memory and the device.
+
+The reference bounds memory by processing one batch element at a time
+(operator.py:59-75) and keeps "one copy of the projection data and volume
+data".  Here the host<->device traffic of a host-resident call
+is split into view chunks so copies overlap the kernels:
+
+* forward  (host volume -> host sinogram): the volume goes up once, then
+  chunk k of views is projected on the compute stream while chunk k-1 is
+  copied down on a copy stream into pinned host memory;
+* back     (host sinogram -> host volume): chunk k+1 of views is copied up on
+  the copy stream while chunk k is back-projected into the resident volume
+  with CTP_FLAG_ACCUMULATE; the volume comes down once at the end.
+
+Every chunk is a plan over ``Geometry.with_views`` of a contiguous view
+range, so the arithmetic per view is identical to the unchunked call
+(forward: bitwise; back: the per-voxel view sum is split into chunk partial
+sums, i.e. a different fp32 summation order).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+
+from . import _native
+
+#: target bytes of sinogram per chunk (host<->device granularity)
+CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def view_chunks(nv: int, view_bytes: int, chunk_bytes: int = CHUNK_BYTES):
+    """Contiguous [a, b) view ranges of about ``chunk_bytes`` each."""
+    per = max(1, min(nv, chunk_bytes // max(1, view_bytes)))
+    n = math.ceil(nv / per)
+    per = math.ceil(nv / n)
+    return [(a, min(nv, a + per)) for a in range(0, nv, per)]
+
+
+def chunk_plans(plan: "_native.Plan", ranges):
+    g, spec, dev = plan.geometry, plan.spec, plan.device.index
+    if len(ranges) == 1:
+        return [plan]
+    return [_native.get_plan(g.with_views(range(a, b)), spec, dev) for a, b in ranges]
+
+
+def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CHUNK_BYTES):
+    """Apply A (direction 0) / A^T (1) to a host f32 tensor [B, ...]; returns
+    a pinned host tensor."""
+    torch = _torch()
+    dev = plan.device
+    B = int(host.shape[0])
+    nv, nr, nc = plan.sino_shape
+    view_bytes = nr * nc * 4
+    ranges = view_chunks(nv, view_bytes, chunk_bytes)
+    plans = chunk_plans(plan, ranges)
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    src = host if host.is_pinned() else host.pin_memory()
+    with torch.cuda.device(dev):
+        if direction == 0:
+            out = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, pin_memory=True)
+            xd = src.to(dev, non_blocking=True)
+            for b in range(B):
+                pending = []
+                for (a, e), p in zip(ranges, plans):
+                    yd = p.forward(xd[b:b + 1])
+                    ev = torch.cuda.Event()
+                    ev.record(compute)
+                    copy.wait_event(ev)
+                    with torch.cuda.stream(copy):
+                        out[b, a:e].copy_(yd[0], non_blocking=True)
+                        yd.record_stream(copy)
+                    pending.append(yd)
+            compute.wait_stream(copy)
+            compute.synchronize()
+            return out
+        out_d = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, device=dev)
+        for b in range(B):
+            for k, ((a, e), p) in enumerate(zip(ranges, plans)):
+                with torch.cuda.stream(copy):
+                    yd = src[b:b + 1, a:e].to(dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                compute.wait_event(ev)
+                yd.record_stream(compute)
+                p.back(yd, out=out_d[b:b + 1], accumulate=k > 0)
+        out = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, pin_memory=True)
+        out.copy_(out_d, non_blocking=True)
+        compute.synchronize()
+        return out

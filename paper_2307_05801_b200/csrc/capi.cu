@@ -1,0 +1,391 @@
+// capi.cu -- extern "C" boundary of libctproj_b200.so (include/ctproj_b200.h).
+//
+// Host side of the drop-in: validates the flattened geometry (what
+// kernel_geom()/pose_table() produce, _common.py:8-39, geometry.py:227-263),
+// digests it in float64 into per-view footprint coefficients (ViewCoef,
+// sf_common.cuh) that stay resident on the device, and launches the SF
+// kernels stream-ordered.  No host synchronisation on the hot path.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ctproj_b200.h"
+#include "sf_common.cuh"
+#include "sf_launch.h"
+
+using ctp::GridParams;
+using ctp::ViewCoef;
+
+struct ctp_plan {
+  ctp_geom geom;               // scalars (poses pointer cleared)
+  std::vector<double> poses;   // host copy, nv*15
+  int device;
+  ViewCoef* d_coef;            // device, nv entries
+  GridParams gp;
+  size_t vol_elems, sino_elems;
+  cudaEvent_t ev[2][2];        // [direction][start/stop], created lazily
+  bool ev_recorded[2];
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? CTP_ERR_OUT_OF_MEMORY : CTP_ERR_CUDA;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && dev >= 0 && dev != prev) {
+      err = cudaSetDevice(dev);
+      switched = (err == cudaSuccess);
+    }
+  }
+  ~DeviceGuard() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
+
+int validate(const ctp_geom* g) {
+  if (!g) return fail(CTP_ERR_INVALID_ARGUMENT, "geometry pointer is null");
+  if (g->kind < CTP_PARALLEL || g->kind > CTP_MODULAR)
+    return fail(CTP_ERR_INVALID_ARGUMENT, "unknown geometry kind");
+  if (g->num_views < 1 || g->num_rows < 1 || g->num_cols < 1)
+    return fail(CTP_ERR_INVALID_ARGUMENT, "detector/view counts must be >= 1");
+  if (g->num_x < 1 || g->num_y < 1 || g->num_z < 1)
+    return fail(CTP_ERR_INVALID_ARGUMENT, "voxel counts must be >= 1");
+  if (!(g->pixel_width > 0 && g->pixel_height > 0))
+    return fail(CTP_ERR_INVALID_ARGUMENT, "pixel sizes must be > 0");
+  if (!(g->voxel_width > 0 && g->voxel_height > 0))
+    return fail(CTP_ERR_INVALID_ARGUMENT, "voxel sizes must be > 0");
+  if ((g->kind == CTP_CONE_FLAT || g->kind == CTP_CONE_CURVED) && !(g->sdd > 0))
+    return fail(CTP_ERR_INVALID_ARGUMENT, "cone geometry requires sdd > 0");
+  if (!g->poses) return fail(CTP_ERR_INVALID_ARGUMENT, "pose table pointer is null");
+  if (g->num_x > 65535 || g->num_y > 65535)
+    return fail(CTP_ERR_INVALID_ARGUMENT, "grid too large (nx, ny <= 65535)");
+  const long long nvox = (long long)g->num_x * g->num_y * g->num_z;
+  const long long nsino = (long long)g->num_views * g->num_rows * g->num_cols;
+  if (nvox >= (1LL << 40) || nsino >= (1LL << 40))
+    return fail(CTP_ERR_INVALID_ARGUMENT, "array too large");
+  for (long long k = 0; k < 15LL * g->num_views; ++k)
+    if (!std::isfinite(g->poses[k])) return fail(CTP_ERR_INVALID_ARGUMENT, "non-finite pose entry");
+  return CTP_OK;
+}
+
+// float64 digestion of one view's pose into affine footprint coefficients
+// over centred grid-index coordinates (see sf_common.cuh for the frame).
+void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>& out) {
+  const double hx = g.voxel_width, hz = g.voxel_height;
+  const double pw = g.pixel_width, ph = g.pixel_height, cr = g.center_row, cc = g.center_col;
+  const double xm = g.x0 + 0.5 * g.num_x * hx, ym = g.y0 + 0.5 * g.num_y * hx;
+  const double half_x = 0.5 * g.num_x, half_y = 0.5 * g.num_y;
+  out.assign(g.num_views, ViewCoef{});
+  for (int v = 0; v < g.num_views; ++v) {
+    const double* s = P + 15 * v;
+    const double* c0 = s + 3;
+    const double* u = s + 6;
+    const double* vax = s + 9;
+    const double* w = s + 12;
+    ViewCoef& c = out[v];
+    c.ux = (float)u[0];
+    c.uy = (float)u[1];
+    c.wx = (float)w[0];
+    c.wy = (float)w[1];
+    c.xs = (float)((s[0] - xm) / hx);
+    c.ys = (float)((s[1] - ym) / hx);
+    c.xc0 = (float)((c0[0] - xm) / hx);
+    c.yc0 = (float)((c0[1] - ym) / hx);
+    if (g.kind == CTP_PARALLEL) {
+      // s = (p - c0).u at z = 0 (_kernels.py:457-460), T = tcen/ph + cr (:621-625)
+      c.na = (float)(((xm - c0[0]) * u[0] + (ym - c0[1]) * u[1] - c0[2] * u[2]) / pw + cc);
+      c.nb = (float)(hx * u[0] / pw);
+      c.nc = (float)(hx * u[1] / pw);
+      c.ta = (float)(((xm - c0[0]) * vax[0] + (ym - c0[1]) * vax[1] +
+                      (g.z0 + 0.5 * hz - c0[2]) * vax[2]) / ph + cr);
+      c.tb = (float)(hx * vax[0] / ph);
+      c.tc = (float)(hx * vax[1] / ph);
+      c.tz = (float)(hz * vax[2] / ph);
+      c.cull = 1;
+      continue;
+    }
+    // cone: plane normal and lamnum (_kernels.py:562-569)
+    const double nxv = u[1] * vax[2] - u[2] * vax[1];
+    const double nyv = u[2] * vax[0] - u[0] * vax[2];
+    const double nzv = u[0] * vax[1] - u[1] * vax[0];
+    const double lamnum = (c0[0] - s[0]) * nxv + (c0[1] - s[1]) * nyv + (c0[2] - s[2]) * nzv;
+    c.dxa = (float)(xm - s[0]);
+    c.dya = (float)(ym - s[1]);
+    c.zc0 = (float)(g.z0 + 0.5 * hz - s[2]);
+    if (g.kind == CTP_CONE_FLAT) {
+      c.na = (float)((xm - s[0]) * u[0] + (ym - s[1]) * u[1] - s[2] * u[2]);
+      c.nb = (float)(hx * u[0]);
+      c.nc = (float)(hx * u[1]);
+      c.da = (float)((xm - s[0]) * nxv + (ym - s[1]) * nyv - s[2] * nzv);
+      c.db = (float)(hx * nxv);
+      c.dc = (float)(hx * nyv);
+      c.dm = (float)((xm - s[0]) * nxv + (ym - s[1]) * nyv);
+      c.s0 = (float)(((s[0] - c0[0]) * u[0] + (s[1] - c0[1]) * u[1] + (s[2] - c0[2]) * u[2]) / pw + cc);
+      c.g = (float)(lamnum / pw);
+      c.lamnum = (float)lamnum;
+    } else {  // curved: s = sdd * atan2(e.u, e.w) (_kernels.py:478-497)
+      c.na = (float)((xm - s[0]) * u[0] + (ym - s[1]) * u[1]);
+      c.nb = (float)(hx * u[0]);
+      c.nc = (float)(hx * u[1]);
+      c.da = (float)((xm - s[0]) * w[0] + (ym - s[1]) * w[1]);
+      c.db = (float)(hx * w[0]);
+      c.dc = (float)(hx * w[1]);
+      c.s0 = (float)cc;
+      c.g = (float)(g.sdd / pw);
+      c.lamnum = (float)g.sdd;
+    }
+    // wedge culling assumes the source lies outside the grid footprint
+    const bool inside = std::fabs((s[0] - xm) / hx) < half_x + 2.0 &&
+                        std::fabs((s[1] - ym) / hx) < half_y + 2.0;
+    c.cull = inside ? 0 : 1;
+  }
+}
+
+GridParams make_grid_params(const ctp_geom& g) {
+  GridParams gp{};
+  gp.kind = g.kind;
+  gp.nv = g.num_views;
+  gp.nr = g.num_rows;
+  gp.nc = g.num_cols;
+  gp.nx = g.num_x;
+  gp.ny = g.num_y;
+  gp.nz = g.num_z;
+  gp.batch = 1;
+  gp.hx = (float)g.voxel_width;
+  gp.hz = (float)g.voxel_height;
+  gp.pw = (float)g.pixel_width;
+  gp.ph = (float)g.pixel_height;
+  gp.cr = (float)g.center_row;
+  gp.cc = (float)g.center_col;
+  gp.sdd = (float)g.sdd;
+  gp.half_x = 0.5f * (float)g.num_x;
+  gp.half_y = 0.5f * (float)g.num_y;
+  gp.inv_ph = (float)(1.0 / g.pixel_height);
+  gp.hz_over_ph = (float)(g.voxel_height / g.pixel_height);
+  gp.e_par = (float)(0.5 * g.voxel_height / g.pixel_height);
+  return gp;
+}
+
+size_t align_up(size_t n) { return (n + 255) & ~size_t(255); }
+
+int check_run_args(const ctp_plan* plan, const void* in, const void* out, int batch,
+                   void* ws, size_t ws_bytes, size_t need) {
+  if (!plan) return fail(CTP_ERR_INVALID_ARGUMENT, "plan is null");
+  if (!in || !out) return fail(CTP_ERR_INVALID_ARGUMENT, "null data pointer");
+  if (batch < 1) return fail(CTP_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (in == out) return fail(CTP_ERR_INVALID_ARGUMENT, "input and output must not alias");
+  if (plan->geom.kind == CTP_MODULAR)
+    return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
+                "separable-footprint projector does not support modular geometry");
+  if (ws_bytes < need || (need > 0 && !ws))
+    return fail(CTP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  return CTP_OK;
+}
+
+// record an event pair around the projector kernel when timing is requested
+struct KernelTimer {
+  ctp_plan* p;
+  int dir;
+  cudaStream_t s;
+  bool on;
+  KernelTimer(const ctp_plan* plan, int direction, cudaStream_t st, uint32_t flags)
+      : p(const_cast<ctp_plan*>(plan)), dir(direction), s(st), on((flags & CTP_FLAG_TIME_KERNEL) != 0) {
+    if (!on) return;
+    for (int k = 0; k < 2; ++k)
+      if (!p->ev[dir][k]) cudaEventCreate(&p->ev[dir][k]);
+    cudaEventRecord(p->ev[dir][0], s);
+  }
+  void stop() {
+    if (!on) return;
+    cudaEventRecord(p->ev[dir][1], s);
+    p->ev_recorded[dir] = true;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int ctp_abi_version(void) { return CTP_ABI_VERSION; }
+
+const char* ctp_status_string(int status) {
+  switch (status) {
+    case CTP_OK: return "ok";
+    case CTP_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case CTP_ERR_UNSUPPORTED_GEOMETRY: return "unsupported geometry";
+    case CTP_ERR_SPEC_MISMATCH: return "spec mismatch";
+    case CTP_ERR_CUDA: return "CUDA runtime error";
+    case CTP_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case CTP_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int ctp_last_error(char* buf, size_t buf_bytes) {
+  if (!buf || buf_bytes == 0) return CTP_ERR_INVALID_ARGUMENT;
+  std::snprintf(buf, buf_bytes, "%s", g_last_error.c_str());
+  return CTP_OK;
+}
+
+int ctp_plan_create(const ctp_geom* geom, int device, ctp_plan** plan_out) {
+  if (!plan_out) return fail(CTP_ERR_INVALID_ARGUMENT, "plan_out is null");
+  *plan_out = nullptr;
+  int st = validate(geom);
+  if (st != CTP_OK) return st;
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  ctp_plan* p = new (std::nothrow) ctp_plan();
+  if (!p) return fail(CTP_ERR_OUT_OF_MEMORY, "host allocation failed");
+  p->geom = *geom;
+  p->geom.poses = nullptr;
+  p->poses.assign(geom->poses, geom->poses + 15 * (size_t)geom->num_views);
+  cudaGetDevice(&p->device);
+  p->gp = make_grid_params(*geom);
+  p->vol_elems = (size_t)geom->num_x * geom->num_y * geom->num_z;
+  p->sino_elems = (size_t)geom->num_views * geom->num_rows * geom->num_cols;
+  std::vector<ViewCoef> coefs;
+  build_view_coefs(*geom, p->poses.data(), coefs);
+  cudaError_t e = cudaMalloc(&p->d_coef, sizeof(ViewCoef) * coefs.size());
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaMalloc(view coefficients)");
+  }
+  e = cudaMemcpy(p->d_coef, coefs.data(), sizeof(ViewCoef) * coefs.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(p->d_coef);
+    delete p;
+    return cuda_fail(e, "upload view coefficients");
+  }
+  *plan_out = p;
+  return CTP_OK;
+}
+
+int ctp_plan_destroy(ctp_plan* plan) {
+  if (!plan) return CTP_OK;
+  DeviceGuard guard(plan->device);
+  if (plan->d_coef) cudaFree(plan->d_coef);
+  for (int d = 0; d < 2; ++d)
+    for (int k = 0; k < 2; ++k)
+      if (plan->ev[d][k]) cudaEventDestroy(plan->ev[d][k]);
+  delete plan;
+  return CTP_OK;
+}
+
+int ctp_plan_shape(const ctp_plan* plan, int64_t* vol_elems, int64_t* sino_elems) {
+  if (!plan) return fail(CTP_ERR_INVALID_ARGUMENT, "plan is null");
+  if (vol_elems) *vol_elems = (int64_t)plan->vol_elems;
+  if (sino_elems) *sino_elems = (int64_t)plan->sino_elems;
+  return CTP_OK;
+}
+
+size_t ctp_sf_workspace_bytes(const ctp_plan* plan, int direction, int batch) {
+  if (!plan || batch < 1) return 0;
+  const size_t per = direction == 0 ? plan->vol_elems : plan->sino_elems;
+  return align_up(per * sizeof(float) * (size_t)batch);
+}
+
+int ctp_sf_forward(const ctp_plan* plan, const float* vol, float* sino, int batch, void* workspace,
+                   size_t workspace_bytes, uint32_t flags, void* stream) {
+  const size_t need = plan ? ctp_sf_workspace_bytes(plan, 0, batch) : 0;
+  int st = check_run_args(plan, vol, sino, batch, workspace, workspace_bytes, need);
+  if (st != CTP_OK) return st;
+  DeviceGuard guard(plan->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const GridParams& gp = plan->gp;
+  float* xT = static_cast<float*>(workspace);
+  cudaError_t e = ctp::launch_transpose(vol, xT, gp.nz, gp.nx * gp.ny, batch, s);
+  if (e != cudaSuccess) return cuda_fail(e, "transpose volume");
+  KernelTimer timer(plan, 0, s, flags);
+  e = ctp::launch_forward(gp, plan->d_coef, xT, sino, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  timer.stop();
+  if (e != cudaSuccess) return cuda_fail(e, "sf_forward_kernel");
+  return CTP_OK;
+}
+
+int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, void* workspace,
+                size_t workspace_bytes, uint32_t flags, void* stream) {
+  const size_t need = plan ? ctp_sf_workspace_bytes(plan, 1, batch) : 0;
+  int st = check_run_args(plan, sino, vol, batch, workspace, workspace_bytes, need);
+  if (st != CTP_OK) return st;
+  DeviceGuard guard(plan->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const GridParams& gp = plan->gp;
+  float* yT = static_cast<float*>(workspace);
+  cudaError_t e = ctp::launch_transpose(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
+  if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram");
+  KernelTimer timer(plan, 1, s, flags);
+  e = ctp::launch_back(gp, plan->d_coef, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  timer.stop();
+  if (e != cudaSuccess) return cuda_fail(e, "sf_back_kernel");
+  return CTP_OK;
+}
+
+int ctp_plan_kernel_time_ms(const ctp_plan* plan, int direction, float* ms) {
+  if (!plan || !ms || direction < 0 || direction > 1)
+    return fail(CTP_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!plan->ev_recorded[direction])
+    return fail(CTP_ERR_INVALID_ARGUMENT, "no timed launch recorded for this direction");
+  DeviceGuard guard(plan->device);
+  cudaError_t e = cudaEventSynchronize(plan->ev[direction][1]);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+  e = cudaEventElapsedTime(ms, plan->ev[direction][0], plan->ev[direction][1]);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+  return CTP_OK;
+}
+
+static int oneshot(const ctp_geom* geom, const float* in, float* out, int batch, void* stream,
+                   int direction) {
+  ctp_plan* plan = nullptr;
+  int st = ctp_plan_create(geom, -1, &plan);
+  if (st != CTP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t need = ctp_sf_workspace_bytes(plan, direction, batch);
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, need, s);
+  if (e != cudaSuccess) {
+    ctp_plan_destroy(plan);
+    return cuda_fail(e, "cudaMallocAsync(workspace)");
+  }
+  st = direction == 0 ? ctp_sf_forward(plan, in, out, batch, ws, need, 0, stream)
+                      : ctp_sf_back(plan, in, out, batch, ws, need, 0, stream);
+  cudaFreeAsync(ws, s);
+  e = cudaStreamSynchronize(s);
+  ctp_plan_destroy(plan);
+  if (st != CTP_OK) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+  return CTP_OK;
+}
+
+int ctp_sf_forward_oneshot(const ctp_geom* geom, const float* vol, float* sino, int batch,
+                           void* stream) {
+  return oneshot(geom, vol, sino, batch, stream, 0);
+}
+
+int ctp_sf_back_oneshot(const ctp_geom* geom, const float* sino, float* vol, int batch,
+                        void* stream) {
+  return oneshot(geom, sino, vol, batch, stream, 1);
+}
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+// sf_common.cuh -- shared host/device definitions of the SF-TR projector pair.
+//
+// The forward (ray-driven gather) and back (voxel-driven gather) kernels both
+// evaluate the separable-footprint coefficient
+//
+//     a(voxel, view, row, col) = (amp * tt(row)) * ts(col)
+//
+// of the reference (_kernels.py:555-647 forward, 666-763 back) through the
+// functions in this header.  Every floating-point step of the coefficient is
+// written with explicit-rounding intrinsics (__fmul_rn, __fadd_rn, __fmaf_rn,
+// ...) so that nvcc cannot contract or reassociate it differently in the two
+// kernels: the pair is then an exact transpose in fp32 (the explicit-matrix
+// test, pkg/tests/test_sf.py:89-111, holds bitwise).
+//
+// Coordinates.  Geometry is pre-digested on the host in float64 (ctp_plan)
+// into per-view affine coefficients over CENTRED GRID-INDEX coordinates
+// (X, Y) = (ix + 0.5 - nx/2, iy + 0.5 - ny/2) for voxel centres (corners sit
+// at half-integers of that frame).  Detector coordinates are expressed in
+// pixel units: column coordinate S = s/pw + cc, row coordinate T = t/ph + cr,
+// so detector column c covers [c - 0.5, c + 0.5] and row r covers
+// [r - 0.5, r + 0.5].  Keeping magnitudes small (|X|,|Y| <= n/2, |S|,|T| <=
+// n_det) holds fp32 rounding of the footprint edges near 1e-5 pixel.
+#pragma once
+
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace ctp {
+
+enum Kind : int { kParallel = 0, kConeFlat = 1, kConeCurved = 2, kModular = 3 };
+
+// Per-view coefficient block (built on the host in f64 by build_view_coefs in
+// capi.cu; 32 floats = 128 B, read with broadcast loads).
+struct alignas(16) ViewCoef {
+  // transverse numerator, affine in (X, Y).  parallel: S itself;
+  // flat: r.u with r = p - src at z = 0; curved: r.u (xy only)
+  float na, nb, nc;
+  // transverse denominator.  flat: r.n (n = u x vax, incl. the z term of
+  // _flat_plane_s); curved: r.w (xy only).  parallel: unused
+  float da, db, dc;
+  float dm;      // flat: centre denominator constant (rcx*nxv + rcy*nyv, no z term)
+  float s0;      // column offset (flat: (src-c0).u/pw + cc; curved: cc)
+  float g;       // flat: lamnum/pw; curved: sdd/pw
+  float lamnum;  // flat: (c0-src).n ; curved: sdd
+  float dxa, dya;  // centre offset from the source in mm: xm - sx, ym - sy
+  float zc0;       // cone: z of the first slice centre minus source z (mm)
+  float ta, tb, tc, tz;  // parallel axial map T = ta + tb X + tc Y + tz iz
+  float ux, uy;          // detector transverse axis (split-axis choice, ray setup)
+  float wx, wy;          // central ray direction (parallel lxy, curved ax test)
+  float xs, ys;          // source in centred grid-index coords
+  float xc0, yc0;        // detector reference point c0 in centred grid-index coords
+  int cull;              // 1: wedge culling is safe for this view (source outside grid)
+  float pad[4];
+};
+static_assert(sizeof(ViewCoef) == 128, "ViewCoef must stay 128 bytes");
+
+// Launch-invariant scalars.
+struct GridParams {
+  int kind;
+  int nv, nr, nc;
+  int nx, ny, nz;
+  int batch;
+  float hx, hz;        // voxel pitches (mm)
+  float pw, ph;        // pixel pitches (mm)
+  float cr, cc;        // detector centre (pixels)
+  float sdd;
+  float half_x, half_y;  // nx/2, ny/2
+  float inv_ph;          // 1/ph
+  float hz_over_ph;      // hz/ph
+  float e_par;           // parallel axial half-width: 0.5*hz/ph
+};
+
+// One (sub-)voxel column's footprint in one view.
+struct SubFoot {
+  float t0, t1, t2, t3;  // sorted transverse breakpoints (column units)
+  float A, B, E;         // axial: T(iz) = A + B*iz, half-width E (row units)
+  float lxy, a0, a1;     // amp(iz) = lxy * sqrt(1 + (a0 + a1*iz)^2)
+  int cl, ch;            // clamped detector-column range (cl > ch: none)
+};
+
+#ifdef __CUDACC__
+
+// ---- explicit-rounding helpers (no contraction across kernels) ------------
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+// hardware sqrt approximation: deterministic, ~1 ulp; amplitude only
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float affine_(float a, float b, float c, float X, float Y) {
+  return fma_(c, Y, fma_(b, X, a));
+}
+
+// _sort4, _kernels.py:393-405 (same comparator network, branch-free)
+__device__ __forceinline__ void sort4f(float& a, float& b, float& c, float& d) {
+  float lo, hi;
+  lo = fminf(a, b); hi = fmaxf(a, b); a = lo; b = hi;
+  lo = fminf(c, d); hi = fmaxf(c, d); c = lo; d = hi;
+  lo = fminf(a, c); hi = fmaxf(a, c); a = lo; c = hi;
+  lo = fminf(b, d); hi = fmaxf(b, d); b = lo; d = hi;
+  lo = fminf(b, c); hi = fmaxf(b, c); b = lo; c = hi;
+}
+
+// _trap_cum, _kernels.py:408-420, in column units: integral of the unit
+// trapezoid (t0..t3) from t0 up to s.
+__device__ __forceinline__ float trap_cum(const SubFoot& f, float s) {
+  if (s <= f.t0) return 0.0f;
+  const float w01 = sub_(f.t1, f.t0), w23 = sub_(f.t3, f.t2);
+  const float full = add_(add_(mul_(0.5f, w01), sub_(f.t2, f.t1)), mul_(0.5f, w23));
+  if (s >= f.t3) return full;
+  if (s < f.t1) {
+    const float d = sub_(s, f.t0);
+    return div_(mul_(mul_(0.5f, d), d), w01);
+  }
+  if (s < f.t2) return add_(mul_(0.5f, w01), sub_(s, f.t1));
+  const float d = sub_(f.t3, s);
+  return sub_(full, div_(mul_(mul_(0.5f, d), d), w23));
+}
+
+// Column weight T_s(col) = (F(col+0.5) - F(col-0.5)) (the /pw of
+// _kernels.py:610-614 is implicit in column units).
+__device__ __forceinline__ float col_weight(const SubFoot& f, int col) {
+  const float c = (float)col;
+  return sub_(trap_cum(f, add_(c, 0.5f)), trap_cum(f, sub_(c, 0.5f)));
+}
+
+// Axial row-overlap T_t(row) of slice iz (_kernels.py:638-644), row units.
+__device__ __forceinline__ float row_center(const SubFoot& f, int iz) {
+  return fma_(f.B, (float)iz, f.A);
+}
+__device__ __forceinline__ float row_overlap(float lo, float hi, int row) {
+  const float r = (float)row;
+  const float a = fmaxf(lo, sub_(r, 0.5f));
+  const float b = fminf(hi, add_(r, 0.5f));
+  return fmaxf(sub_(b, a), 0.0f);
+}
+// SF amplitude (_sf_amplitude, _kernels.py:529-539): lxy / cos(axial tilt)
+__device__ __forceinline__ float amplitude(const SubFoot& f, int iz) {
+  const float q = fma_(f.a1, (float)iz, f.a0);
+  return mul_(f.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+}
+
+// _sf_transverse (_kernels.py:441-526) + axial setup for one sub-voxel whose
+// centre is (X, Y) (centred grid-index coords) with half-widths (hxi, hyi) in
+// index units.  Returns false on the reference's ok=False paths.
+__device__ __forceinline__ bool sub_footprint(const ViewCoef& v, const GridParams& gp,
+                                              float X, float Y, float hxi, float hyi,
+                                              SubFoot& f) {
+  const float xa = sub_(X, hxi), xb = add_(X, hxi);
+  const float ya = sub_(Y, hyi), yb = add_(Y, hyi);
+  const float hxw = mul_(hxi, gp.hx), hyw = mul_(hyi, gp.hx);  // world half-widths
+  float s0, s1, s2, s3, dxn, dyn;
+  if (gp.kind == kParallel) {
+    s0 = affine_(v.na, v.nb, v.nc, xa, ya);
+    s1 = affine_(v.na, v.nb, v.nc, xb, ya);
+    s2 = affine_(v.na, v.nb, v.nc, xa, yb);
+    s3 = affine_(v.na, v.nb, v.nc, xb, yb);
+    dxn = v.wx;
+    dyn = v.wy;
+    f.A = affine_(v.ta, v.tb, v.tc, X, Y);
+    f.B = v.tz;
+    f.E = gp.e_par;
+    f.a0 = 0.0f;
+    f.a1 = 0.0f;
+  } else {
+    const float dx = fma_(gp.hx, X, v.dxa), dy = fma_(gp.hx, Y, v.dya);
+    const float rho = __fsqrt_rn(fma_(dx, dx, mul_(dy, dy)));
+    if (!(rho >= 1e-9f)) return false;
+    float mag;
+    if (gp.kind == kConeCurved) {
+      if (!(fma_(dx, v.wx, mul_(dy, v.wy)) > 0.0f)) return false;
+      mag = div_(gp.sdd, rho);
+      s0 = fma_(v.g, atan2f(affine_(v.na, v.nb, v.nc, xa, ya), affine_(v.da, v.db, v.dc, xa, ya)), v.s0);
+      s1 = fma_(v.g, atan2f(affine_(v.na, v.nb, v.nc, xb, ya), affine_(v.da, v.db, v.dc, xb, ya)), v.s0);
+      s2 = fma_(v.g, atan2f(affine_(v.na, v.nb, v.nc, xa, yb), affine_(v.da, v.db, v.dc, xa, yb)), v.s0);
+      s3 = fma_(v.g, atan2f(affine_(v.na, v.nb, v.nc, xb, yb), affine_(v.da, v.db, v.dc, xb, yb)), v.s0);
+    } else {
+      // flat panel: ray/plane intersection (_flat_plane_s, _kernels.py:423-438)
+      float d[4], n[4];
+      d[0] = affine_(v.da, v.db, v.dc, xa, ya); n[0] = affine_(v.na, v.nb, v.nc, xa, ya);
+      d[1] = affine_(v.da, v.db, v.dc, xb, ya); n[1] = affine_(v.na, v.nb, v.nc, xb, ya);
+      d[2] = affine_(v.da, v.db, v.dc, xa, yb); n[2] = affine_(v.na, v.nb, v.nc, xa, yb);
+      d[3] = affine_(v.da, v.db, v.dc, xb, yb); n[3] = affine_(v.na, v.nb, v.nc, xb, yb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!(fabsf(d[k]) > 1e-12f)) return false;
+        if (!(div_(v.lamnum, d[k]) > 0.0f)) return false;
+      }
+      s0 = fma_(v.g, div_(n[0], d[0]), v.s0);
+      s1 = fma_(v.g, div_(n[1], d[1]), v.s0);
+      s2 = fma_(v.g, div_(n[2], d[2]), v.s0);
+      s3 = fma_(v.g, div_(n[3], d[3]), v.s0);
+      const float den = affine_(v.dm, v.db, v.dc, X, Y);
+      if (!(fabsf(den) > 1e-12f)) return false;
+      mag = div_(v.lamnum, den);
+      if (!(mag > 0.0f)) return false;
+    }
+    dxn = div_(dx, rho);
+    dyn = div_(dy, rho);
+    // axial: tcen = mag*(cz - src_z)  (_kernels.py:626-628), in row units
+    const float bm = mul_(mag, gp.hz_over_ph);
+    f.B = bm;
+    f.E = mul_(0.5f, bm);
+    f.A = fma_(mul_(mag, v.zc0), gp.inv_ph, gp.cr);
+    f.a0 = div_(v.zc0, rho);
+    f.a1 = div_(gp.hz, rho);
+  }
+  sort4f(s0, s1, s2, s3);
+  f.t0 = s0; f.t1 = s1; f.t2 = s2; f.t3 = s3;
+  const float big = 1.0e30f;
+  const float la = fabsf(dxn) > 1e-12f ? div_(mul_(2.0f, hxw), fabsf(dxn)) : big;
+  const float lb = fabsf(dyn) > 1e-12f ? div_(mul_(2.0f, hyw), fabsf(dyn)) : big;
+  f.lxy = fminf(la, lb);
+  int cl = (int)ceilf(sub_(s0, 0.5f));
+  int ch = (int)floorf(add_(s3, 0.5f));
+  f.cl = cl < 0 ? 0 : cl;
+  f.ch = ch > gp.nc - 1 ? gp.nc - 1 : ch;
+  return true;
+}
+
+// Full voxel column (ix, iy) in one view, with the >8-column split of
+// _sf_subdivide (_kernels.py:542-552) and the sub-voxel loop of
+// _kernels.py:582-601.  Returns a bit mask of valid sub-footprints:
+// 1 = s0 only (no split), bits 0/1 = halves of a split voxel (in the
+// reference's sub order), 0 = the voxel contributes nothing in this view.
+__device__ __forceinline__ int column_footprint(const ViewCoef& v, const GridParams& gp,
+                                                int ix, int iy, SubFoot& s0, SubFoot& s1) {
+  const float X = sub_((float)ix + 0.5f, gp.half_x);
+  const float Y = sub_((float)iy + 0.5f, gp.half_y);
+  if (!sub_footprint(v, gp, X, Y, 0.5f, 0.5f, s0)) return 0;
+  if (!(sub_(s0.t3, s0.t0) > 8.0f)) return 1;
+  const bool along_x = fabsf(v.ux) >= fabsf(v.uy);
+  const float hxi = along_x ? 0.25f : 0.5f, hyi = along_x ? 0.5f : 0.25f;
+  const float X0 = along_x ? sub_(X, 0.25f) : X, Y0 = along_x ? Y : sub_(Y, 0.25f);
+  const float X1 = along_x ? add_(X, 0.25f) : X, Y1 = along_x ? Y : add_(Y, 0.25f);
+  int mask = 0;
+  if (sub_footprint(v, gp, X0, Y0, hxi, hyi, s0)) mask |= 1;
+  if (sub_footprint(v, gp, X1, Y1, hxi, hyi, s1)) mask |= 2;
+  return mask;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace ctp

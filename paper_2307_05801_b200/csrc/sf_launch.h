@@ -1,0 +1,23 @@
+// sf_launch.h -- internal launcher interface between the C-ABI (capi.cu) and
+// the kernels (sf_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "sf_common.cuh"
+
+namespace ctp {
+
+cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batch,
+                             cudaStream_t st);
+// xT: volume in [batch][ny*nx][nz] layout; sino: [batch][nv][nr][nc]
+cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const float* xT,
+                           float* sino, int batch, bool accumulate, cudaStream_t st);
+// yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]
+cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
+                        int batch, bool accumulate, cudaStream_t st);
+size_t forward_smem_bytes(int n_primary);
+
+}  // namespace ctp

@@ -1,0 +1,219 @@
+"""GPU parity of the SF pair against the reference (golden fixtures) and the
+CPU oracle, through the C-ABI library.
+
+Bars (north_star): rel-L2 <= 1e-4 and max-abs <= 1e-4 * max|ref| for forward
+and back projections; adjoint dot-product test <= 1e-5 relative; explicit
+fp32 matrices exactly transposed (A == B^T bitwise, the fp32 analogue of
+pkg/tests/test_sf.py:89-111's 1e-9 bound).
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2307_05801_b200 as ct
+from paper_2307_05801_b200 import _native
+
+from conftest import ADJOINT_TOL, MAX_ABS_TOL, REL_L2_TOL, load_golden, max_abs_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+CASES = sorted(n for n in load_golden() if not n.startswith("explicit"))
+EXPLICIT = sorted(n for n in load_golden() if n.startswith("explicit"))
+
+
+def pair_of(cfg):
+    g, spec = ct.parse_config(json.dumps(cfg))
+    return ct.ProjectorPair(ct.SF, g, spec)
+
+
+def dev_fwd(P, x):
+    return ct.forward(P, torch.as_tensor(x, device=DEV).reshape((-1,) + P.volumeSpec.shape))
+
+
+def dev_back(P, y):
+    return ct.adjoint(P, torch.as_tensor(y, device=DEV).reshape((-1,) + P.geometry.shape))
+
+
+def test_native_library_is_loaded():
+    lib = _native.load_library()
+    assert lib.ctp_abi_version() == _native.ABI_VERSION
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_forward_matches_reference(golden, name):
+    c = golden[name]
+    P = pair_of(c["config"])
+    got = dev_fwd(P, c["x"])[0].cpu().numpy()
+    assert rel_l2(got, c["fwd"]) <= REL_L2_TOL, rel_l2(got, c["fwd"])
+    assert max_abs_rel(got, c["fwd"]) <= MAX_ABS_TOL, max_abs_rel(got, c["fwd"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_back_matches_reference(golden, name):
+    c = golden[name]
+    P = pair_of(c["config"])
+    got = dev_back(P, c["y"])[0].cpu().numpy()
+    assert rel_l2(got, c["back"]) <= REL_L2_TOL, rel_l2(got, c["back"])
+    assert max_abs_rel(got, c["back"]) <= MAX_ABS_TOL, max_abs_rel(got, c["back"])
+
+
+@pytest.mark.parametrize("name", EXPLICIT)
+def test_explicit_matrices_exact_transpose(golden, name):
+    c = golden[name]
+    P = pair_of(c["config"])
+    n = P.volumeSpec.num_voxels
+    m = int(np.prod(P.geometry.shape))
+    A = dev_fwd(P, torch.eye(n, device=DEV)).reshape(n, m).T.cpu().numpy()
+    B = dev_back(P, torch.eye(m, device=DEV)).reshape(m, n).T.cpu().numpy()
+    # the fp32 pair is an exact transpose
+    assert np.array_equal(A, B.T), np.abs(A - B.T).max()
+    # and matches the reference's f64-computed matrix to fp32 accuracy
+    assert np.abs(A - c["A"]).max() <= 1e-5 * np.abs(c["A"]).max()
+
+
+@pytest.mark.parametrize("name", ["parallel_small", "cone_small", "curved_small", "offset_cone",
+                                  "split_cone", "fan_like"])
+def test_adjoint_check(golden, name):
+    P = pair_of(golden[name]["config"])
+    rep = ct.adjoint_check(P, trials=5, seed=0)
+    assert rep["maxRelErr"] < ADJOINT_TOL, rep
+
+
+def test_batch_equals_separate_calls_and_is_deterministic(golden):
+    c = golden["cone_small"]
+    P = pair_of(c["config"])
+    x = torch.rand((3,) + P.volumeSpec.shape, device=DEV)
+    yb = ct.forward(P, x)
+    for i in range(3):
+        assert torch.equal(yb[i], ct.forward(P, x[i:i + 1])[0])
+    assert torch.equal(yb, ct.forward(P, x))
+    y = torch.rand((3,) + P.geometry.shape, device=DEV)
+    xb = ct.adjoint(P, y)
+    for i in range(3):
+        assert torch.equal(xb[i], ct.adjoint(P, y[i:i + 1])[0])
+    assert torch.equal(xb, ct.adjoint(P, y))
+
+
+def test_host_path_matches_device_path(golden):
+    c = golden["offset_cone"]
+    P = pair_of(c["config"])
+    x = c["x"][None]
+    host = ct.forward(P, x)
+    assert isinstance(host, np.ndarray)
+    dev = dev_fwd(P, x).cpu().numpy()
+    assert np.array_equal(host, dev)
+    yh = ct.adjoint(P, c["y"][None])
+    yd = dev_back(P, c["y"]).cpu().numpy()
+    assert np.array_equal(yh, yd)
+
+
+def test_chunked_host_path(golden):
+    from paper_2307_05801_b200 import chunking
+
+    c = golden["cone_small"]
+    P = pair_of(c["config"])
+    plan = P.plan(0)
+    xh = torch.from_numpy(c["x"][None].copy())
+    yh = torch.from_numpy(c["y"][None].copy())
+    one = chunking.host_apply(plan, xh, 0)
+    many = chunking.host_apply(plan, xh, 0, chunk_bytes=16 * 16 * 4 * 3)  # 3 views per chunk
+    assert torch.equal(one, many)
+    b1 = chunking.host_apply(plan, yh, 1)
+    b3 = chunking.host_apply(plan, yh, 1, chunk_bytes=16 * 16 * 4 * 3)
+    assert rel_l2(b3.numpy(), b1.numpy()) < 1e-6
+
+
+def test_binding_autograd_is_native_adjoint_bitwise(golden, tmp_path):
+    from paper_2307_05801_b200.ctproj_torch import load_param
+
+    c = golden["parallel_small"]
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps(c["config"]))
+    proj = load_param(cfg)
+    P = proj.pair
+    x = torch.rand((1,) + P.volumeSpec.shape, device=DEV, requires_grad=True)
+    ybar = torch.rand((1,) + P.geometry.shape, device=DEV)
+    y = proj(x)
+    assert torch.equal(y, ct.forward(P, x.detach()))
+    y.backward(ybar)
+    assert torch.equal(x.grad, ct.adjoint(P, ybar))
+    yy = torch.rand((1,) + P.geometry.shape, device=DEV, requires_grad=True)
+    xx = proj.backproject(yy)
+    xbar = torch.rand((1,) + P.volumeSpec.shape, device=DEV)
+    xx.backward(xbar)
+    assert torch.equal(yy.grad, ct.forward(P, xbar))
+    # CPU tensors are accepted and give the same numbers
+    xc = x.detach().cpu()
+    assert torch.equal(proj(xc), y.detach().cpu())
+
+
+def test_training_loop_decreases_loss(golden):
+    from paper_2307_05801_b200.ctproj_torch import Projector
+
+    c = golden["cone_small"]
+    proj = Projector(pair_of(c["config"]))
+    truth = torch.from_numpy(c["x"]).to(DEV)[None]
+    with torch.no_grad():
+        target = proj(truth)
+    x = torch.zeros_like(truth, requires_grad=True)
+    opt = torch.optim.SGD([x], lr=2e-4)
+    losses = []
+    for _ in range(30):
+        opt.zero_grad()
+        loss = 0.5 * ((proj(x) - target) ** 2).sum()
+        loss.backward()
+        opt.step()
+        losses.append(loss.item())
+    assert losses[-1] < 0.5 * losses[0]
+    assert sum(b < a for a, b in zip(losses, losses[1:])) >= 27
+
+
+# ---------------------------------------------------------------------------
+# the BASELINE configs against the oracle (full geometry, view subsets)
+# ---------------------------------------------------------------------------
+C1 = dict(geometry="parallel", numX=128, numY=128, numZ=128, voxelWidth=1.0, voxelHeight=1.0,
+          numRows=128, numCols=128, pixelHeight=1.0, pixelWidth=1.0, numAngles=180,
+          angularRange=180.0)
+C3 = dict(geometry="cone", numX=512, numY=512, numZ=512, voxelWidth=0.6667, voxelHeight=0.6667,
+          numRows=768, numCols=768, pixelHeight=1.0, pixelWidth=1.0, sod=1000.0, sdd=1500.0,
+          numAngles=720, angularRange=360.0)
+C2 = dict(geometry="cone", numX=512, numY=512, numZ=1, voxelWidth=0.6667, voxelHeight=1.0,
+          numRows=1, numCols=768, pixelHeight=1.0, pixelWidth=1.0, sod=1000.0, sdd=1500.0,
+          numAngles=720, angularRange=360.0)
+
+
+def _parity(oracle_mod, cfg, batch=1, views=None):
+    if views is not None:
+        from oracle import oracle as o
+
+        cfg = o.with_views(cfg, views)
+    P = pair_of(cfg)
+    rng = np.random.default_rng(0)
+    x = rng.random((batch,) + P.volumeSpec.shape, dtype=np.float32)
+    y = np.random.default_rng(1).random((batch,) + P.geometry.shape, dtype=np.float32)
+    fx = dev_fwd(P, x).cpu().numpy()
+    by = dev_back(P, y).cpu().numpy()
+    for b in range(batch):
+        rf = oracle_mod.sf_forward(cfg, x[b])
+        rb = oracle_mod.sf_back(cfg, y[b])
+        assert rel_l2(fx[b], rf) <= REL_L2_TOL and max_abs_rel(fx[b], rf) <= MAX_ABS_TOL, \
+            (rel_l2(fx[b], rf), max_abs_rel(fx[b], rf))
+        assert rel_l2(by[b], rb) <= REL_L2_TOL and max_abs_rel(by[b], rb) <= MAX_ABS_TOL, \
+            (rel_l2(by[b], rb), max_abs_rel(by[b], rb))
+    return P
+
+
+def test_c1_parallel_full(oracle_mod):
+    _parity(oracle_mod, C1)
+
+
+def test_c3_cone_view_subset(oracle_mod):
+    _parity(oracle_mod, C3, views=[0, 97, 181, 500])
+
+
+def test_c2_fan_batch_subset(oracle_mod):
+    _parity(oracle_mod, C2, batch=2, views=list(range(0, 720, 8)))
