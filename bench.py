@@ -213,8 +213,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--views", type=int, default=0,
+                    help="profiling only: restrict to the first N views (not a bench number)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.views:
+        cfg["numAngles"] = args.views
+        cfg["angularRange"] = cfg["angularRange"] * args.views / CONFIGS[args.config]["numAngles"]
     if args.impl == "reference":
         return run_reference(args, cfg)
 

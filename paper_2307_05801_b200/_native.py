@@ -29,7 +29,7 @@ from .errors import (
 from .geometry import Geometry, VolumeSpec, kernel_args
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libctproj_b200.so")
+LIB_PATH = os.environ.get("CTPROJ_LIB") or os.path.join(_HERE, "csrc", "libctproj_b200.so")
 ABI_VERSION = 1
 
 CTP_OK = 0

@@ -111,6 +111,8 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
     c.ys = (float)((s[1] - ym) / hx);
     c.xc0 = (float)((c0[0] - xm) / hx);
     c.yc0 = (float)((c0[1] - ym) / hx);
+    // _sf_subdivide (_kernels.py:550): the tie at 45 deg must be broken in f64
+    c.split_x = (std::fabs(u[0]) * hx >= std::fabs(u[1]) * hx) ? 1 : 0;
     if (g.kind == CTP_PARALLEL) {
       // s = (p - c0).u at z = 0 (_kernels.py:457-460), T = tcen/ph + cr (:621-625)
       c.na = (float)(((xm - c0[0]) * u[0] + (ym - c0[1]) * u[1] - c0[2] * u[2]) / pw + cc);

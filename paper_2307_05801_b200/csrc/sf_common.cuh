@@ -55,7 +55,8 @@ struct alignas(16) ViewCoef {
   float xs, ys;          // source in centred grid-index coords
   float xc0, yc0;        // detector reference point c0 in centred grid-index coords
   int cull;              // 1: wedge culling is safe for this view (source outside grid)
-  float pad[4];
+  int split_x;           // _sf_subdivide axis decided in f64: |u_x| hx >= |u_y| hx
+  float pad[3];
 };
 static_assert(sizeof(ViewCoef) == 128, "ViewCoef must stay 128 bytes");
 
@@ -111,39 +112,68 @@ __device__ __forceinline__ void sort4f(float& a, float& b, float& c, float& d) {
   lo = fminf(b, c); hi = fmaxf(b, c); b = lo; c = hi;
 }
 
-// _trap_cum, _kernels.py:408-420, in column units: integral of the unit
-// trapezoid (t0..t3) from t0 up to s.
-__device__ __forceinline__ float trap_cum(const SubFoot& f, float s) {
-  if (s <= f.t0) return 0.0f;
+// _trap_cum, _kernels.py:408-420, in column units, branch-free (the setup is
+// evaluated lane-parallel over views, so branches would diverge): integral of
+// the unit trapezoid (t0..t3) from t0 up to s, as rising + flat + falling parts
+//   L = 0.5 (a - t0)^2 / (t1 - t0),              a = clamp(s, t0, t1)
+//   M = b - t1,                                  b = clamp(s, t1, t2)
+//   R = (c - t2) ((t3 - c) + (t3 - t2)) / (2 (t3 - t2)),  c = clamp(s, t2, t3)
+// Degenerate edges (t0 == t1 or t2 == t3) use a zero reciprocal.
+struct Trap {
+  float t0, t1, t2, t3;
+  float i01, i23;  // 0.5/(t1-t0), 0.5/(t3-t2) (0 when degenerate)
+};
+__device__ __forceinline__ Trap make_trap(const SubFoot& f) {
+  Trap p;
+  p.t0 = f.t0; p.t1 = f.t1; p.t2 = f.t2; p.t3 = f.t3;
   const float w01 = sub_(f.t1, f.t0), w23 = sub_(f.t3, f.t2);
-  const float full = add_(add_(mul_(0.5f, w01), sub_(f.t2, f.t1)), mul_(0.5f, w23));
-  if (s >= f.t3) return full;
-  if (s < f.t1) {
-    const float d = sub_(s, f.t0);
-    return div_(mul_(mul_(0.5f, d), d), w01);
-  }
-  if (s < f.t2) return add_(mul_(0.5f, w01), sub_(s, f.t1));
-  const float d = sub_(f.t3, s);
-  return sub_(full, div_(mul_(mul_(0.5f, d), d), w23));
+  p.i01 = w01 > 0.0f ? div_(0.5f, w01) : 0.0f;
+  p.i23 = w23 > 0.0f ? div_(0.5f, w23) : 0.0f;
+  return p;
+}
+__device__ __forceinline__ float clampf_(float x, float lo, float hi) {
+  return fminf(fmaxf(x, lo), hi);
+}
+__device__ __forceinline__ float trap_cum(const Trap& p, float s) {
+  const float a = sub_(clampf_(s, p.t0, p.t1), p.t0);
+  const float b = sub_(clampf_(s, p.t1, p.t2), p.t1);
+  const float c = clampf_(s, p.t2, p.t3);
+  const float L = mul_(mul_(a, a), p.i01);
+  const float R = mul_(mul_(sub_(c, p.t2), add_(sub_(p.t3, c), sub_(p.t3, p.t2))), p.i23);
+  return add_(add_(L, b), R);
 }
 
-// Column weight T_s(col) = (F(col+0.5) - F(col-0.5)) (the /pw of
+// Column weight T_s(col) = F(col+0.5) - F(col-0.5) (the /pw of
 // _kernels.py:610-614 is implicit in column units).
-__device__ __forceinline__ float col_weight(const SubFoot& f, int col) {
+__device__ __forceinline__ float col_weight(const Trap& p, int col) {
   const float c = (float)col;
-  return sub_(trap_cum(f, add_(c, 0.5f)), trap_cum(f, sub_(c, 0.5f)));
+  return sub_(trap_cum(p, add_(c, 0.5f)), trap_cum(p, sub_(c, 0.5f)));
 }
 
-// Axial row-overlap T_t(row) of slice iz (_kernels.py:638-644), row units.
+// Axial map (_kernels.py:619-645) in row units: slice iz spans
+// [T - E, T + E] with T = A + B iz; its weight in row r is the overlap with
+// [r - 0.5, r + 0.5] written as a difference of clamped boundaries,
+//   tt(r) = clamp(r + 0.5, lo, hi) - clamp(r - 0.5, lo, hi),
+// which both kernels evaluate identically (r +- 0.5 is exact in fp32).
 __device__ __forceinline__ float row_center(const SubFoot& f, int iz) {
   return fma_(f.B, (float)iz, f.A);
 }
 __device__ __forceinline__ float row_overlap(float lo, float hi, int row) {
   const float r = (float)row;
-  const float a = fmaxf(lo, sub_(r, 0.5f));
-  const float b = fminf(hi, add_(r, 0.5f));
-  return fmaxf(sub_(b, a), 0.0f);
+  return sub_(clampf_(add_(r, 0.5f), lo, hi), clampf_(sub_(r, 0.5f), lo, hi));
 }
+// First row whose interval can overlap [lo, hi]: min{ r : r + 0.5 > lo },
+// computed exactly (so rows below it have exactly zero overlap).
+__device__ __forceinline__ int first_row(float lo) {
+  int r = (int)floorf(add_(lo, 0.5f));
+  if (!((float)r + 0.5f > lo)) r += 1;
+  else if ((float)r - 0.5f > lo) r -= 1;
+  return r;
+}
+// Rows a slice of axial height 2E = B can touch, counted from first_row
+// (with a 1e-3 margin against fp32 rounding of lo / hi).
+__device__ __forceinline__ int rows_per_slice(float B) { return (int)(B + 1.001f) + 1; }
+
 // SF amplitude (_sf_amplitude, _kernels.py:529-539): lxy / cos(axial tilt)
 __device__ __forceinline__ float amplitude(const SubFoot& f, int iz) {
   const float q = fma_(f.a1, (float)iz, f.a0);
@@ -239,7 +269,7 @@ __device__ __forceinline__ int column_footprint(const ViewCoef& v, const GridPar
   const float Y = sub_((float)iy + 0.5f, gp.half_y);
   if (!sub_footprint(v, gp, X, Y, 0.5f, 0.5f, s0)) return 0;
   if (!(sub_(s0.t3, s0.t0) > 8.0f)) return 1;
-  const bool along_x = fabsf(v.ux) >= fabsf(v.uy);
+  const bool along_x = v.split_x != 0;
   const float hxi = along_x ? 0.25f : 0.5f, hyi = along_x ? 0.5f : 0.25f;
   const float X0 = along_x ? sub_(X, 0.25f) : X, Y0 = along_x ? Y : sub_(Y, 0.25f);
   const float X1 = along_x ? add_(X, 0.25f) : X, Y1 = along_x ? Y : add_(Y, 0.25f);

@@ -1,26 +1,40 @@
 // sf_kernels.cu -- sm_100a kernels of the SF-TR projector pair.
 //
-//   sf_forward_kernel : y = A x,  ray-driven GATHER.  One CTA owns a detector
-//                       tile (view v, FW_CW columns, FW_ROWS rows) and gathers
-//                       every voxel column whose footprint reaches the tile
-//                       (reference: voxel-driven scatter into an f64 scratch
-//                       per view, _kernels.py:555-663).
-//   sf_back_kernel    : x = A^T y, voxel-driven GATHER.  One warp owns one
-//                       voxel column x BK_ZC slices, lanes along z, and loops
-//                       over all views (reference: _kernels.py:666-763).
-//   transpose_kernel  : [batch][R][C] -> [batch][C][R] layout change used to
-//                       make the z (volume) / row (sinogram) axis contiguous.
+//   sf_back_kernel    : x = A^T y, voxel-driven GATHER (reference:
+//                       sf_back_kernel, _kernels.py:666-763).  One warp owns one
+//                       voxel column x BK_ZC slices (lanes along z) and loops
+//                       over all views.  Footprint setup is LANE-PARALLEL: lane l
+//                       sets up view vb+l, so one instruction stream prepares 32
+//                       views; the per-view work is then a row-sum table
+//                       Q(r) = sum_c ts(c) y[v][c][r] (coalesced, lanes along r)
+//                       and K = rows_per_slice(B) fused multiply-adds per voxel.
+//   sf_forward_kernel : y = A x, ray-driven GATHER (reference: per-view scatter
+//                       into an f64 scratch, _kernels.py:555-663).  One CTA owns
+//                       a detector tile (view, FW_CW columns, FW_ROWS rows),
+//                       enumerates the voxel columns of the wedge that reaches
+//                       the tile, sets them up one per thread, and each warp
+//                       gathers its 32*FW_KR rows: P(r) = sum_iz tt(r,iz) amp x,
+//                       y(r,c) += ts(c) P(r).
+//   transpose_kernel  : [batch][R][C] -> [batch][C][R] layout change making the
+//                       z (volume) / row (sinogram) axis contiguous.
 //
-// No atomics anywhere; every output element is produced by exactly one
-// thread with a fixed summation order, so results are deterministic.
-// Both kernels take the footprint coefficients from sf_common.cuh so that the
-// pair is an exact fp32 transpose (see that header).
+// No atomics; every output element has one owner thread and a fixed
+// summation order, so results are deterministic run to run.  Both kernels
+// evaluate the coefficient (amp*tt)*ts from sf_common.cuh with identical
+// operations, so the pair is an exact fp32 transpose.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "sf_common.cuh"
 #include "sf_launch.h"
+
+#ifndef CTP_BK_MINB
+#define CTP_BK_MINB 3  // resident CTAs/SM the back kernel is register-budgeted for
+#endif
+#ifndef CTP_FW_MINB
+#define CTP_FW_MINB 3
+#endif
 
 namespace ctp {
 
@@ -48,77 +62,95 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
   }
 }
 
+// Column weights of NW consecutive detector columns c_first.. : NW+1 shared
+// boundary evaluations of the trapezoid integral.  ts(c) = F(c+.5) - F(c-.5)
+// with exactly the same F values wherever a boundary is shared, so any caller
+// (back: footprint columns, forward: tile columns) gets bitwise equal weights.
+template <int NW>
+__device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&ts)[NW]) {
+  float prev = trap_cum(p, sub_((float)c_first, 0.5f));
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const float cur = trap_cum(p, add_((float)(c_first + k), 0.5f));
+    ts[k] = sub_(cur, prev);
+    prev = cur;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // back projection: x = A^T y
 // ---------------------------------------------------------------------------
 constexpr int BK_WARPS = 8;
-constexpr int BK_ZPL = 4;              // voxels per lane
-constexpr int BK_ZC = 32 * BK_ZPL;     // slices per warp
-constexpr int BK_QBUF = 640;           // per-warp Q staging (rows)
-constexpr int BK_MAXC = 8;             // footprint columns kept in registers
+constexpr int BK_ZPL = 4;           // voxels per lane
+constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
+constexpr int BK_QMAX = 352;        // per-warp row-sum table (rows)
+constexpr int BK_NCF = 4;           // footprint columns handled by the fast path
 
-// Q(r) = sum_c ts(c) * y[v][c][r]  (column sum first; fixed ascending-c order)
-__device__ __forceinline__ float q_value(const SubFoot& f, const float (&ts)[BK_MAXC], int ncols,
-                                         const float* __restrict__ yv, int nr, int r) {
-  float q = 0.0f;
-  if (ncols <= BK_MAXC) {
+struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
+  float A, B, E, lxy;
+  float a0, a1;
+  int cl, ncol;  // ncol <= 0: no contribution
+  float ts[BK_NCF];
+  float t0, t1, t2, t3;  // breakpoints, for footprints wider than BK_NCF columns
+};
+static_assert(sizeof(BkEntry) == 64, "BkEntry layout");
+
+__device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f) {
+  e.A = f.A; e.B = f.B; e.E = f.E; e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
+  e.cl = f.cl;
+  e.ncol = f.ch - f.cl + 1;
+  e.t0 = f.t0; e.t1 = f.t1; e.t2 = f.t2; e.t3 = f.t3;
+  const Trap p = make_trap(f);
+  float ts[BK_NCF];
+  col_weights<BK_NCF>(p, f.cl, ts);
 #pragma unroll
-    for (int k = 0; k < BK_MAXC; ++k)
-      if (k < ncols) q = fma_(ts[k], __ldg(yv + (size_t)(f.cl + k) * nr + r), q);
-  } else {
-    for (int c = f.cl; c <= f.ch; ++c) q = fma_(col_weight(f, c), __ldg(yv + (size_t)c * nr + r), q);
+  for (int k = 0; k < BK_NCF; ++k) e.ts[k] = ts[k];
+}
+
+// generic row sum for wide footprints (computes ts on the fly, same order)
+__device__ __forceinline__ float q_wide(const BkEntry& e, const float* __restrict__ yv, int nr, int r) {
+  SubFoot f;
+  f.t0 = e.t0; f.t1 = e.t1; f.t2 = e.t2; f.t3 = e.t3;
+  const Trap p = make_trap(f);
+  float q = 0.0f;
+  float prev = trap_cum(p, sub_((float)e.cl, 0.5f));
+  for (int k = 0; k < e.ncol; ++k) {
+    const float cur = trap_cum(p, add_((float)(e.cl + k), 0.5f));
+    q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + k) * nr + r), q);
+    prev = cur;
   }
   return q;
 }
 
-__device__ __forceinline__ void back_sub(const SubFoot& f, const GridParams& gp,
-                                         const float* __restrict__ yv, float* qw, int lane,
-                                         int izs, int ize, float (&acc)[BK_ZPL]) {
-  if (f.cl > f.ch) return;
-  const int nr = gp.nr;
-  int Ra = (int)floorf(sub_(sub_(row_center(f, izs), f.E), 0.5f));
-  int Rb = (int)ceilf(add_(add_(row_center(f, ize), f.E), 0.5f));
-  Ra = Ra < 0 ? 0 : Ra;
-  Rb = Rb > nr - 1 ? nr - 1 : Rb;
-  if (Ra > Rb) return;
-  const int nq = Rb - Ra + 1;
-  const int ncols = f.ch - f.cl + 1;
-  float ts[BK_MAXC];
+__device__ __forceinline__ float q_fast(const BkEntry& e, const float* __restrict__ yv, int nr, int r) {
+  float q = 0.0f;
 #pragma unroll
-  for (int k = 0; k < BK_MAXC; ++k) ts[k] = (k < ncols) ? col_weight(f, f.cl + k) : 0.0f;
-  const bool table = nq <= BK_QBUF;
-  if (table) {
-    for (int j = lane; j < nq; j += 32) qw[j] = q_value(f, ts, ncols, yv, nr, Ra + j);
-    __syncwarp();
-  }
-#pragma unroll
-  for (int m = 0; m < BK_ZPL; ++m) {
-    const int iz = izs + lane + 32 * m;
-    if (iz > ize) continue;
-    const float T = row_center(f, iz);
-    const float lo = sub_(T, f.E), hi = add_(T, f.E);
-    const float amp = amplitude(f, iz);
-    int r0 = (int)floorf(sub_(lo, 0.5f));
-    int r1 = (int)ceilf(add_(hi, 0.5f));
-    r0 = r0 < Ra ? Ra : r0;
-    r1 = r1 > Rb ? Rb : r1;
-    float a = acc[m];
-    for (int r = r0; r <= r1; ++r) {
-      const float tt = row_overlap(lo, hi, r);
-      const float q = table ? qw[r - Ra] : q_value(f, ts, ncols, yv, nr, r);
-      a = fma_(mul_(amp, tt), q, a);
-    }
-    acc[m] = a;
-  }
-  if (table) __syncwarp();
+  for (int k = 0; k < BK_NCF; ++k)
+    if (k < e.ncol) q = fma_(e.ts[k], __ldg(yv + (size_t)(e.cl + k) * nr + r), q);
+  return q;
 }
 
-__global__ void __launch_bounds__(BK_WARPS * 32) sf_back_kernel(GridParams gp,
+// accumulate the K rows of one voxel: acc += sum_k (amp*tt_k) * Q(r0+k)
+template <int K>
+__device__ __forceinline__ float gather_rows(float acc, float amp, float lo, float hi, int r0,
+                                             const float* q) {
+  float g = clampf_(sub_((float)r0, 0.5f), lo, hi);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float gn = clampf_(add_((float)(r0 + k), 0.5f), lo, hi);
+    acc = fma_(mul_(amp, sub_(gn, g)), q[k], acc);
+    g = gn;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(GridParams gp,
                                                                 const ViewCoef* __restrict__ vcoef,
                                                                 const float* __restrict__ yT,
                                                                 float* __restrict__ out,
                                                                 int accumulate) {
-  __shared__ float qbuf[BK_WARPS][BK_QBUF];
+  __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
+  __shared__ float qbuf[BK_WARPS][BK_QMAX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbx = (gp.nx + 3) >> 2;
   const int ix = (blockIdx.x % nbx) * 4 + (warp & 3);
@@ -127,21 +159,86 @@ __global__ void __launch_bounds__(BK_WARPS * 32) sf_back_kernel(GridParams gp,
   const int b = blockIdx.z;
   const int izs = blockIdx.y * BK_ZC;
   const int ize = min(izs + BK_ZC, gp.nz) - 1;
-  const size_t sino_elems = (size_t)gp.nv * gp.nr * gp.nc;
-  const float* yb = yT + (size_t)b * sino_elems;
+  const int nr = gp.nr;
+  const size_t view_elems = (size_t)gp.nc * nr;
+  const float* yb = yT + (size_t)b * gp.nv * view_elems;
   float* qw = qbuf[warp];
+  BkEntry(&my)[32][2] = ents[warp];
   float acc[BK_ZPL];
 #pragma unroll
   for (int m = 0; m < BK_ZPL; ++m) acc[m] = 0.0f;
 
-  for (int v = 0; v < gp.nv; ++v) {
-    const ViewCoef vc = vcoef[v];
-    SubFoot f0, f1;
-    const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
-    if (mask == 0) continue;
-    const float* yv = yb + (size_t)v * gp.nc * gp.nr;  // [c][r] of view v
-    if (mask & 1) back_sub(f0, gp, yv, qw, lane, izs, ize, acc);
-    if (mask & 2) back_sub(f1, gp, yv, qw, lane, izs, ize, acc);
+  for (int vb = 0; vb < gp.nv; vb += 32) {
+    // ---- lane-parallel footprint setup: lane l <- view vb + l
+    {
+      const int v = vb + lane;
+      BkEntry e0, e1;
+      e0.ncol = 0;
+      e1.ncol = 0;
+      if (v < gp.nv) {
+        const ViewCoef vc = vcoef[v];
+        SubFoot f0, f1;
+        const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
+        if (mask & 1) fill_entry(e0, f0);
+        if (mask & 2) fill_entry(e1, f1);
+      }
+      my[lane][0] = e0;
+      my[lane][1] = e1;
+    }
+    __syncwarp();
+    const int nvb = min(32, gp.nv - vb);
+    for (int j = 0; j < nvb; ++j) {
+#pragma unroll 1
+      for (int s = 0; s < 2; ++s) {
+        const BkEntry e = my[j][s];
+        if (e.ncol <= 0) continue;
+        const int K = rows_per_slice(e.B);
+        const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
+        const int Rz = first_row(sub_(fma_(e.B, (float)ize, e.A), e.E)) + K - 1;
+        if (Rz < 0 || Ra > nr - 1) continue;
+        const float* yv = yb + (size_t)(vb + j) * view_elems;  // [c][r] of the view
+        const int nq = Rz - Ra + 1;
+        const bool table = nq <= BK_QMAX && e.ncol <= BK_NCF && K <= 4;
+        if (table) {
+          for (int t = lane; t < nq; t += 32) {
+            const int r = Ra + t;
+            qw[t] = (r >= 0 && r < nr) ? q_fast(e, yv, nr, r) : 0.0f;
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int m = 0; m < BK_ZPL; ++m) {
+          const int iz = izs + lane + 32 * m;
+          if (iz > ize) continue;
+          const float T = fma_(e.B, (float)iz, e.A);
+          const float lo = sub_(T, e.E), hi = add_(T, e.E);
+          const float q = fma_(e.a1, (float)iz, e.a0);
+          const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+          const int r0 = first_row(lo);
+          if (table) {
+            const float* qp = qw + (r0 - Ra);
+            if (K == 2) acc[m] = gather_rows<2>(acc[m], amp, lo, hi, r0, qp);
+            else if (K == 3) acc[m] = gather_rows<3>(acc[m], amp, lo, hi, r0, qp);
+            else acc[m] = gather_rows<4>(acc[m], amp, lo, hi, r0, qp);
+          } else {
+            // generic: any K, any footprint width, rows read directly
+            float a = acc[m];
+            float g = clampf_(sub_((float)r0, 0.5f), lo, hi);
+            for (int k = 0; k < K; ++k) {
+              const int r = r0 + k;
+              const float gn = clampf_(add_((float)r, 0.5f), lo, hi);
+              float qv = 0.0f;
+              if (r >= 0 && r < nr) qv = e.ncol <= BK_NCF ? q_fast(e, yv, nr, r) : q_wide(e, yv, nr, r);
+              a = fma_(mul_(amp, sub_(gn, g)), qv, a);
+              g = gn;
+            }
+            acc[m] = a;
+          }
+        }
+        if (table) __syncwarp();
+      }
+    }
+    __syncwarp();
   }
   // out[b][iz][iy][ix]
   const size_t plane = (size_t)gp.ny * gp.nx;
@@ -160,23 +257,23 @@ __global__ void __launch_bounds__(BK_WARPS * 32) sf_back_kernel(GridParams gp,
 // ---------------------------------------------------------------------------
 constexpr int FW_WARPS = 8;
 constexpr int FW_THREADS = FW_WARPS * 32;
-constexpr int FW_CW = 8;                      // detector columns per tile
-constexpr int FW_KR = 3;                      // 32-row groups per warp
+constexpr int FW_CW = 8;                        // detector columns per tile
+constexpr int FW_KR = 3;                        // 32-row groups per warp
 constexpr int FW_ROWS = FW_WARPS * 32 * FW_KR;  // rows per tile
-constexpr int FW_BATCH = FW_THREADS;          // candidate columns per setup round
-constexpr int FW_VBUF = 256;                  // per-warp amp*x staging (slices)
+constexpr int FW_BATCH = FW_THREADS;            // candidate columns per setup round
+constexpr int FW_VBUF = 160;                    // per-warp slice staging (lo, hi, amp*x)
 
 struct FwEntry {
-  int col;        // iy*nx + ix
-  float A, B, E;  // axial map
+  int ixy;    // (iy << 16) | ix
+  int cinfo;  // first tile column offset | (count << 8)
+  float A, B, E;
   float lxy, a0, a1;
-  float invB;
-  float ts[FW_CW];  // transverse weights of the tile's columns (0 outside [cl,ch])
+  float ts[FW_CW];  // weights of the tile's columns (0 outside the footprint)
 };
 static_assert(sizeof(FwEntry) == 64, "FwEntry layout");
 
 size_t forward_smem_bytes(int n_primary) {
-  return sizeof(FwEntry) * 2 * FW_BATCH + sizeof(float) * FW_WARPS * FW_VBUF +
+  return sizeof(FwEntry) * 2 * FW_BATCH + sizeof(float4) * FW_WARPS * FW_VBUF +
          sizeof(int) * (2 * (size_t)n_primary + 2) + sizeof(int) * 2 * (FW_WARPS + 1);
 }
 
@@ -188,16 +285,21 @@ __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams&
   return cols_ok && thi > band_lo && tlo < band_hi;
 }
 
-__device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int col, int c0, int cw) {
-  e.col = col;
+__device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int ix, int iy, int c0,
+                                            int cw) {
+  e.ixy = (iy << 16) | ix;
   e.A = f.A; e.B = f.B; e.E = f.E;
   e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
-  e.invB = 1.0f / f.B;
+  const Trap p = make_trap(f);
+  float ts[FW_CW];
+  col_weights<FW_CW>(p, c0, ts);
+  const int lo = max(f.cl, c0), hi = min(f.ch, c0 + cw - 1);
 #pragma unroll
   for (int c = 0; c < FW_CW; ++c) {
     const int cc = c0 + c;
-    e.ts[c] = (c < cw && cc >= f.cl && cc <= f.ch) ? col_weight(f, cc) : 0.0f;
+    e.ts[c] = (cc >= lo && cc <= hi) ? ts[c] : 0.0f;
   }
+  e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);
 }
 
 // exclusive scan of one int per thread over the CTA; returns the total
@@ -250,14 +352,35 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
   }
 }
 
-__global__ void __launch_bounds__(FW_THREADS) sf_forward_kernel(GridParams gp,
+// y(r, c) += ts(c) * P(r) for the tile columns an entry reaches
+__device__ __forceinline__ void apply_cols(float (&acc)[FW_CW], const FwEntry& E, float P) {
+  const int off = E.cinfo & 0xff, n = E.cinfo >> 8;
+  if (n <= 3) {
+    switch (off) {
+#define CTP_CASE(o)                                                          \
+  case o:                                                                    \
+    acc[o] = fma_(E.ts[o], P, acc[o]);                                       \
+    if (o + 1 < FW_CW) acc[(o + 1) % FW_CW] = fma_(E.ts[(o + 1) % FW_CW], P, acc[(o + 1) % FW_CW]); \
+    if (o + 2 < FW_CW) acc[(o + 2) % FW_CW] = fma_(E.ts[(o + 2) % FW_CW], P, acc[(o + 2) % FW_CW]); \
+    break;
+      CTP_CASE(0) CTP_CASE(1) CTP_CASE(2) CTP_CASE(3) CTP_CASE(4) CTP_CASE(5) CTP_CASE(6) CTP_CASE(7)
+#undef CTP_CASE
+      default: break;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < FW_CW; ++c) acc[c] = fma_(E.ts[c], P, acc[c]);
+  }
+}
+
+__global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(GridParams gp,
                                                                 const ViewCoef* __restrict__ vcoef,
                                                                 const float* __restrict__ xT,
                                                                 float* __restrict__ y,
                                                                 int accumulate, int view_batch0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwEntry* ent = reinterpret_cast<FwEntry*>(smem_raw);
-  float* xabuf = reinterpret_cast<float*>(ent + 2 * FW_BATCH);
+  float4* sbuf = reinterpret_cast<float4*>(ent + 2 * FW_BATCH);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int vb = blockIdx.z + view_batch0;
@@ -275,7 +398,6 @@ __global__ void __launch_bounds__(FW_THREADS) sf_forward_kernel(GridParams gp,
   const bool primary_x = fabsf(dlx) * nl + fabsf(dhx) * nh >= fabsf(dly) * nl + fabsf(dhy) * nh;
   const int nP = primary_x ? gp.nx : gp.ny, nQ = primary_x ? gp.ny : gp.nx;
   const float halfP = primary_x ? gp.half_x : gp.half_y, halfQ = primary_x ? gp.half_y : gp.half_x;
-  // rays as (p, q) = (primary, secondary) components
   const float lp = primary_x ? plx : ply, lq = primary_x ? ply : plx;
   const float ldp = primary_x ? dlx : dly, ldq = primary_x ? dly : dlx;
   const float hp = primary_x ? phx : phy, hq = primary_x ? phy : phx;
@@ -283,9 +405,9 @@ __global__ void __launch_bounds__(FW_THREADS) sf_forward_kernel(GridParams gp,
   const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
   const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
 
-  int* prefix = reinterpret_cast<int*>(xabuf + FW_WARPS * FW_VBUF);  // nP + 1
-  int* jlo = prefix + (nP + 1);                                      // nP
-  int* scan_tmp = jlo + nP + 1;                                      // FW_WARPS + 1
+  int* prefix = reinterpret_cast<int*>(sbuf + FW_WARPS * FW_VBUF);  // nP + 1
+  int* jlo = prefix + (nP + 1);                                     // nP
+  int* scan_tmp = jlo + nP + 1;                                     // FW_WARPS + 1
   const int seg = (nP + FW_THREADS - 1) / FW_THREADS;
   int my_sum = 0;
   for (int t = 0; t < seg; ++t) {
@@ -334,13 +456,13 @@ __global__ void __launch_bounds__(FW_THREADS) sf_forward_kernel(GridParams gp,
   const float band_hi = (float)min(R0 + FW_ROWS, gp.nr) - 0.5f;
   const size_t ncolvox = (size_t)gp.nx * gp.ny;
   const float* xb = xT + (size_t)b * ncolvox * gp.nz;
-  float* xw = xabuf + warp * FW_VBUF;
+  float4* sw = sbuf + warp * FW_VBUF;
 
   for (int base = 0; base < total; base += FW_BATCH) {
     // 2a. one candidate per thread -> footprint setup -> compacted entries
     const int k = base + tid;
     SubFoot f0, f1;
-    int mask = 0, col = 0;
+    int mask = 0, ix = 0, iy = 0;
     if (k < total) {
       int lo = 0, hi = nP;
       while (hi - lo > 1) {
@@ -348,64 +470,67 @@ __global__ void __launch_bounds__(FW_THREADS) sf_forward_kernel(GridParams gp,
         if (prefix[mid] <= k) lo = mid; else hi = mid;
       }
       const int i = lo, j = jlo[i] + (k - prefix[i]);
-      const int ix = primary_x ? i : j, iy = primary_x ? j : i;
-      col = iy * gp.nx + ix;
+      ix = primary_x ? i : j;
+      iy = primary_x ? j : i;
       mask = column_footprint(vc, gp, ix, iy, f0, f1);
-      // keep sub-footprints that reach the tile's columns and row band
       if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
       if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
     }
-    const int cnt = __popc(mask);
     int nent;
-    const int off = block_exclusive_scan(cnt, scan_tmp, nent);
-    if (mask & 1) write_entry(ent[off], f0, col, c0, cw);
-    if (mask & 2) write_entry(ent[off + (mask & 1)], f1, col, c0, cw);
+    const int off = block_exclusive_scan(__popc(mask), scan_tmp, nent);
+    if (mask & 1) write_entry(ent[off], f0, ix, iy, c0, cw);
+    if (mask & 2) write_entry(ent[off + (mask & 1)], f1, ix, iy, c0, cw);
     __syncthreads();
 
     // 2b. every warp gathers every entry into its own rows
     if (rw0 <= rw1) {
       for (int e = 0; e < nent; ++e) {
         const FwEntry& E = ent[e];
-        SubFoot f;
-        f.A = E.A; f.B = E.B; f.E = E.E; f.lxy = E.lxy; f.a0 = E.a0; f.a1 = E.a1;
-        const float invB = E.invB;
+        const float A = E.A, B = E.B, Eh = E.E;
+        const float invB = __fdividef(1.0f, B);
         // slices whose axial interval can reach rows [rw0, rw1]
-        int za = (int)floorf(((float)rw0 - 0.5f - f.E - f.A) * invB) - 1;
-        int zb = (int)ceilf(((float)rw1 + 0.5f + f.E - f.A) * invB) + 1;
+        int za = (int)floorf(((float)rw0 - 0.5f - Eh - A) * invB) - 1;
+        int zb = (int)ceilf(((float)rw1 + 0.5f + Eh - A) * invB) + 1;
         za = max(za, 0);
         zb = min(zb, gp.nz - 1);
         if (za > zb) continue;
-        const float* xc = xb + (size_t)E.col * gp.nz;
+        const int NC = (int)ceilf((1.0f + 2.0f * Eh) * invB) + 2;
+        const float zbase = (-0.5f - Eh - A) * invB;
+        const int col = (E.ixy >> 16) * gp.nx + (E.ixy & 0xffff);
+        const float* xc = xb + (size_t)col * gp.nz;
+        const float lxy = E.lxy, a0 = E.a0, a1 = E.a1;
         float P[FW_KR];
 #pragma unroll
         for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
         for (int piece = za; piece <= zb; piece += FW_VBUF) {
           const int pe = min(piece + FW_VBUF - 1, zb);
-          for (int iz = piece + lane; iz <= pe; iz += 32)
-            xw[iz - piece] = mul_(amplitude(f, iz), __ldg(xc + iz));
+          for (int iz = piece + lane; iz <= pe; iz += 32) {
+            const float T = fma_(B, (float)iz, A);
+            const float q = fma_(a1, (float)iz, a0);
+            const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
+            sw[iz - piece] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + iz)), 0.0f);
+          }
           __syncwarp();
 #pragma unroll
           for (int kk = 0; kk < FW_KR; ++kk) {
             const int r = rw0 + 32 * kk + lane;
             if (r > rw1) continue;
-            int z0 = (int)floorf(((float)r - 0.5f - f.E - f.A) * invB) - 1;
-            int z1 = (int)ceilf(((float)r + 0.5f + f.E - f.A) * invB) + 1;
-            z0 = max(z0, piece);
-            z1 = min(z1, pe);
+            const float rf = (float)r;
+            const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
+            const int cz = (int)floorf(fmaf(rf, invB, zbase)) - 1;
+            const int i0 = max(cz, piece), i1 = min(cz + NC - 1, pe);
             float p = P[kk];
-            for (int iz = z0; iz <= z1; ++iz) {
-              const float T = row_center(f, iz);
-              const float tt = row_overlap(sub_(T, f.E), add_(T, f.E), r);
-              p = fma_(tt, xw[iz - piece], p);
+            for (int i = i0; i <= i1; ++i) {
+              const float4 d = sw[i - piece];
+              const float tt = sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y));
+              p = fma_(tt, d.z, p);
             }
             P[kk] = p;
           }
           __syncwarp();
         }
 #pragma unroll
-        for (int kk = 0; kk < FW_KR; ++kk)
-#pragma unroll
-          for (int c = 0; c < FW_CW; ++c) acc[kk][c] = fma_(E.ts[c], P[kk], acc[kk][c]);
+        for (int kk = 0; kk < FW_KR; ++kk) apply_cols(acc[kk], E, P[kk]);
       }
     }
     __syncthreads();  // entries are overwritten by the next round
