@@ -95,7 +95,7 @@ __device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b)
 // hardware sqrt approximation: deterministic, ~1 ulp; amplitude only
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float affine_(float a, float b, float c, float X, float Y) {
@@ -162,14 +162,14 @@ __device__ __forceinline__ float row_overlap(float lo, float hi, int row) {
   const float r = (float)row;
   return sub_(clampf_(add_(r, 0.5f), lo, hi), clampf_(sub_(r, 0.5f), lo, hi));
 }
-// First row whose interval can overlap [lo, hi]: min{ r : r + 0.5 > lo },
-// computed exactly (so rows below it have exactly zero overlap).
-__device__ __forceinline__ int first_row(float lo) {
-  int r = (int)floorf(add_(lo, 0.5f));
-  if (!((float)r + 0.5f > lo)) r += 1;
-  else if ((float)r - 0.5f > lo) r -= 1;
-  return r;
-}
+// First row whose interval can overlap [lo, hi]: min{ r : r + 0.5 > lo }
+// = floor(lo - 0.5) + 1.  For |lo| < 2^22 the subtraction lo - 0.5 is exact
+// in fp32 (both operands are multiples of ulp(lo) <= 0.5, Sterbenz below 1),
+// so rows below first_row have exactly zero overlap.  row_floor returns
+// floor(lo - 0.5) = r0 - 1 as an integer-valued float; the boundaries of row
+// r0 + k are then row_floor + 0.5 + k and row_floor + 1.5 + k (exact).
+__device__ __forceinline__ float row_floor(float lo) { return floorf(sub_(lo, 0.5f)); }
+__device__ __forceinline__ int first_row(float lo) { return (int)row_floor(lo) + 1; }
 // Rows a slice of axial height 2E = B can touch, counted from first_row
 // (with a 1e-3 margin against fp32 rounding of lo / hi).
 __device__ __forceinline__ int rows_per_slice(float B) { return (int)(B + 1.001f) + 1; }

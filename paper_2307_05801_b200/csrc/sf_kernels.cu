@@ -81,25 +81,24 @@ __device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&
 // back projection: x = A^T y
 // ---------------------------------------------------------------------------
 constexpr int BK_WARPS = 8;
-constexpr int BK_ZPL = 4;           // voxels per lane
+constexpr int BK_ZPL = 8;           // voxels per lane
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
-constexpr int BK_QMAX = 352;        // per-warp row-sum table (rows)
-constexpr int BK_NCF = 4;           // footprint columns handled by the fast path
+constexpr int BK_QMAX = 560;        // per-warp row-sum table (rows): ZC * 2 + margin
+constexpr int BK_NCF = 4;           // footprint columns handled by the table path
 
 struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
   float A, B, E, lxy;
   float a0, a1;
-  int cl, ncol;  // ncol <= 0: no contribution
+  int cl;
+  int ncol;  // 0: no contribution; > BK_NCF: wide footprint (direct path)
   float ts[BK_NCF];
-  float t0, t1, t2, t3;  // breakpoints, for footprints wider than BK_NCF columns
 };
-static_assert(sizeof(BkEntry) == 64, "BkEntry layout");
+static_assert(sizeof(BkEntry) == 48, "BkEntry layout");
 
 __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f) {
   e.A = f.A; e.B = f.B; e.E = f.E; e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
   e.cl = f.cl;
-  e.ncol = f.ch - f.cl + 1;
-  e.t0 = f.t0; e.t1 = f.t1; e.t2 = f.t2; e.t3 = f.t3;
+  e.ncol = f.ch >= f.cl ? f.ch - f.cl + 1 : 0;
   const Trap p = make_trap(f);
   float ts[BK_NCF];
   col_weights<BK_NCF>(p, f.cl, ts);
@@ -107,48 +106,71 @@ __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f) {
   for (int k = 0; k < BK_NCF; ++k) e.ts[k] = ts[k];
 }
 
-// generic row sum for wide footprints (computes ts on the fly, same order)
-__device__ __forceinline__ float q_wide(const BkEntry& e, const float* __restrict__ yv, int nr, int r) {
-  SubFoot f;
-  f.t0 = e.t0; f.t1 = e.t1; f.t2 = e.t2; f.t3 = e.t3;
-  const Trap p = make_trap(f);
-  float q = 0.0f;
-  float prev = trap_cum(p, sub_((float)e.cl, 0.5f));
-  for (int k = 0; k < e.ncol; ++k) {
-    const float cur = trap_cum(p, add_((float)(e.cl + k), 0.5f));
-    q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + k) * nr + r), q);
-    prev = cur;
+// Direct (table-free) contribution of one voxel: rows r0..r0+K-1, any
+// footprint width.  Same operations, in the same order, as the table path.
+__device__ __noinline__ float back_voxel_direct(float acc, float amp, float lo, float hi,
+                                                const BkEntry& e, const Trap& wide, int K,
+                                                const float* __restrict__ yv, int nr) {
+  const float fl = row_floor(lo);  // r0 - 1
+  const int r0 = (int)fl + 1;
+  float g = clampf_(add_(fl, 0.5f), lo, hi);
+  for (int k = 0; k < K; ++k) {
+    const int r = r0 + k;
+    const float gn = clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+    float q = 0.0f;
+    if (r >= 0 && r < nr) {
+      if (e.ncol <= BK_NCF) {
+        for (int c = 0; c < e.ncol; ++c) q = fma_(e.ts[c], __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+      } else {
+        float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
+        for (int c = 0; c < e.ncol; ++c) {
+          const float cur = trap_cum(wide, add_((float)(e.cl + c), 0.5f));
+          q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+          prev = cur;
+        }
+      }
+    }
+    acc = fma_(mul_(amp, sub_(gn, g)), q, acc);
+    g = gn;
   }
-  return q;
+  return acc;
 }
 
-__device__ __forceinline__ float q_fast(const BkEntry& e, const float* __restrict__ yv, int nr, int r) {
-  float q = 0.0f;
-#pragma unroll
-  for (int k = 0; k < BK_NCF; ++k)
-    if (k < e.ncol) q = fma_(e.ts[k], __ldg(yv + (size_t)(e.cl + k) * nr + r), q);
-  return q;
-}
-
-// accumulate the K rows of one voxel: acc += sum_k (amp*tt_k) * Q(r0+k)
+// table path: acc += sum_k (amp * tt_k) * Q(r0 + k), K rows, Q from smem
 template <int K>
-__device__ __forceinline__ float gather_rows(float acc, float amp, float lo, float hi, int r0,
-                                             const float* q) {
-  float g = clampf_(sub_((float)r0, 0.5f), lo, hi);
+__device__ __forceinline__ float back_voxel_rows(float acc, float amp, float lo, float hi,
+                                                 const float* qw, int Ra) {
+  const float fl = row_floor(lo);  // r0 - 1 (integer-valued)
+  const float* q = qw + ((int)fl + 1 - Ra);
+  float g = clampf_(add_(fl, 0.5f), lo, hi);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const float gn = clampf_(add_((float)(r0 + k), 0.5f), lo, hi);
+    const float gn = clampf_(add_(fl, (float)k + 1.5f), lo, hi);
     acc = fma_(mul_(amp, sub_(gn, g)), q[k], acc);
     g = gn;
   }
   return acc;
 }
 
-__global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(GridParams gp,
-                                                                const ViewCoef* __restrict__ vcoef,
-                                                                const float* __restrict__ yT,
-                                                                float* __restrict__ out,
-                                                                int accumulate) {
+template <int K>
+__device__ __forceinline__ void back_slices(float (&acc)[BK_ZPL], const BkEntry& e, float izf0,
+                                            int nvalid, const float* qw, int Ra) {
+#pragma unroll
+  for (int m = 0; m < BK_ZPL; ++m) {
+    if (m < nvalid) {
+      const float izf = izf0 + (float)(32 * m);
+      const float T = fma_(e.B, izf, e.A);
+      const float lo = sub_(T, e.E), hi = add_(T, e.E);
+      const float q = fma_(e.a1, izf, e.a0);
+      const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+      acc[m] = back_voxel_rows<K>(acc[m], amp, lo, hi, qw, Ra);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
+    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
+    float* __restrict__ out, int accumulate) {
   __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
   __shared__ float qbuf[BK_WARPS][BK_QMAX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -159,11 +181,15 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(Gri
   const int b = blockIdx.z;
   const int izs = blockIdx.y * BK_ZC;
   const int ize = min(izs + BK_ZC, gp.nz) - 1;
-  const int nr = gp.nr;
-  const size_t view_elems = (size_t)gp.nc * nr;
+  const int nr = gp.nr, nc = gp.nc;
+  const size_t view_elems = (size_t)nc * nr;
   const float* yb = yT + (size_t)b * gp.nv * view_elems;
   float* qw = qbuf[warp];
   BkEntry(&my)[32][2] = ents[warp];
+  // this lane's slices: izs + lane + 32 m, m < nvalid
+  const int span = ize - izs - lane;  // may be negative when nz < 32
+  const int nvalid = span < 0 ? 0 : min(BK_ZPL, span / 32 + 1);
+  const float izf0 = (float)(izs + lane);
   float acc[BK_ZPL];
 #pragma unroll
   for (int m = 0; m < BK_ZPL; ++m) acc[m] = 0.0f;
@@ -191,51 +217,57 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(Gri
 #pragma unroll 1
       for (int s = 0; s < 2; ++s) {
         const BkEntry e = my[j][s];
-        if (e.ncol <= 0) continue;
+        if (e.ncol == 0) continue;
         const int K = rows_per_slice(e.B);
         const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
         const int Rz = first_row(sub_(fma_(e.B, (float)ize, e.A), e.E)) + K - 1;
         if (Rz < 0 || Ra > nr - 1) continue;
         const float* yv = yb + (size_t)(vb + j) * view_elems;  // [c][r] of the view
         const int nq = Rz - Ra + 1;
-        const bool table = nq <= BK_QMAX && e.ncol <= BK_NCF && K <= 4;
-        if (table) {
+        if (nq <= BK_QMAX && e.ncol <= BK_NCF && K <= 4) {
+          // row sums Q(r) = sum_k ts_k y[cl+k][r]; absent columns have ts = 0 and
+          // read a clamped (valid) column, adding exactly 0
+          const float* p0 = yv + (size_t)e.cl * nr;
+          const float* p1 = yv + (size_t)min(e.cl + 1, nc - 1) * nr;
+          const float* p2 = yv + (size_t)min(e.cl + 2, nc - 1) * nr;
+          const float* p3 = yv + (size_t)min(e.cl + 3, nc - 1) * nr;
+          const float t0 = e.ts[0];
+          const float t1 = e.ncol > 1 ? e.ts[1] : 0.0f;
+          const float t2 = e.ncol > 2 ? e.ts[2] : 0.0f;
+          const float t3 = e.ncol > 3 ? e.ts[3] : 0.0f;
           for (int t = lane; t < nq; t += 32) {
             const int r = Ra + t;
-            qw[t] = (r >= 0 && r < nr) ? q_fast(e, yv, nr, r) : 0.0f;
+            const bool in = (unsigned)r < (unsigned)nr;
+            const int rr = in ? r : 0;
+            float q = fma_(t0, __ldg(p0 + rr), 0.0f);
+            q = fma_(t1, __ldg(p1 + rr), q);
+            q = fma_(t2, __ldg(p2 + rr), q);
+            q = fma_(t3, __ldg(p3 + rr), q);
+            qw[t] = in ? q : 0.0f;
           }
           __syncwarp();
-        }
-#pragma unroll
-        for (int m = 0; m < BK_ZPL; ++m) {
-          const int iz = izs + lane + 32 * m;
-          if (iz > ize) continue;
-          const float T = fma_(e.B, (float)iz, e.A);
-          const float lo = sub_(T, e.E), hi = add_(T, e.E);
-          const float q = fma_(e.a1, (float)iz, e.a0);
-          const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
-          const int r0 = first_row(lo);
-          if (table) {
-            const float* qp = qw + (r0 - Ra);
-            if (K == 2) acc[m] = gather_rows<2>(acc[m], amp, lo, hi, r0, qp);
-            else if (K == 3) acc[m] = gather_rows<3>(acc[m], amp, lo, hi, r0, qp);
-            else acc[m] = gather_rows<4>(acc[m], amp, lo, hi, r0, qp);
-          } else {
-            // generic: any K, any footprint width, rows read directly
-            float a = acc[m];
-            float g = clampf_(sub_((float)r0, 0.5f), lo, hi);
-            for (int k = 0; k < K; ++k) {
-              const int r = r0 + k;
-              const float gn = clampf_(add_((float)r, 0.5f), lo, hi);
-              float qv = 0.0f;
-              if (r >= 0 && r < nr) qv = e.ncol <= BK_NCF ? q_fast(e, yv, nr, r) : q_wide(e, yv, nr, r);
-              a = fma_(mul_(amp, sub_(gn, g)), qv, a);
-              g = gn;
-            }
-            acc[m] = a;
+          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Ra);
+          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, Ra);
+          else back_slices<4>(acc, e, izf0, nvalid, qw, Ra);
+          __syncwarp();
+        } else {
+          Trap wide{};
+          if (e.ncol > BK_NCF) {  // rare: rebuild the breakpoints of this footprint
+            SubFoot f0, f1;
+            const int mask = column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
+            (void)mask;
+            wide = make_trap(s == 0 ? f0 : f1);
+          }
+          for (int m = 0; m < BK_ZPL; ++m) {
+            if (m >= nvalid) break;
+            const float izf = izf0 + (float)(32 * m);
+            const float T = fma_(e.B, izf, e.A);
+            const float lo = sub_(T, e.E), hi = add_(T, e.E);
+            const float q = fma_(e.a1, izf, e.a0);
+            const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+            acc[m] = back_voxel_direct(acc[m], amp, lo, hi, e, wide, K, yv, nr);
           }
         }
-        if (table) __syncwarp();
       }
     }
     __syncwarp();
@@ -245,9 +277,8 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(Gri
   float* ob = out + (size_t)b * plane * gp.nz + (size_t)iy * gp.nx + ix;
 #pragma unroll
   for (int m = 0; m < BK_ZPL; ++m) {
-    const int iz = izs + lane + 32 * m;
-    if (iz > ize) continue;
-    float* p = ob + (size_t)iz * plane;
+    if (m >= nvalid) break;
+    float* p = ob + (size_t)(izs + lane + 32 * m) * plane;
     *p = accumulate ? (*p + acc[m]) : acc[m];
   }
 }
@@ -261,19 +292,24 @@ constexpr int FW_CW = 8;                        // detector columns per tile
 constexpr int FW_KR = 3;                        // 32-row groups per warp
 constexpr int FW_ROWS = FW_WARPS * 32 * FW_KR;  // rows per tile
 constexpr int FW_BATCH = FW_THREADS;            // candidate columns per setup round
-constexpr int FW_VBUF = 160;                    // per-warp slice staging (lo, hi, amp*x)
+constexpr int FW_PAD = 6;                       // zero sentinels on each side of a piece
+constexpr int FW_VBUF = 192;                    // slices staged per warp and piece
+constexpr int FW_SBUF = FW_VBUF + 2 * FW_PAD;
 
 struct FwEntry {
-  int ixy;    // (iy << 16) | ix
+  int col;    // iy*nx + ix
   int cinfo;  // first tile column offset | (count << 8)
   float A, B, E;
   float lxy, a0, a1;
+  float invB, cb;  // candidate slices of row r start at floor(r*invB + cb) + 1
+  int ncand;       // candidate slices per row (covers every nonzero overlap)
+  int pad;
   float ts[FW_CW];  // weights of the tile's columns (0 outside the footprint)
 };
-static_assert(sizeof(FwEntry) == 64, "FwEntry layout");
+static_assert(sizeof(FwEntry) == 80, "FwEntry layout");
 
 size_t forward_smem_bytes(int n_primary) {
-  return sizeof(FwEntry) * 2 * FW_BATCH + sizeof(float4) * FW_WARPS * FW_VBUF +
+  return sizeof(FwEntry) * 2 * FW_BATCH + sizeof(float4) * FW_WARPS * FW_SBUF +
          sizeof(int) * (2 * (size_t)n_primary + 2) + sizeof(int) * 2 * (FW_WARPS + 1);
 }
 
@@ -285,11 +321,17 @@ __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams&
   return cols_ok && thi > band_lo && tlo < band_hi;
 }
 
-__device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int ix, int iy, int c0,
-                                            int cw) {
-  e.ixy = (iy << 16) | ix;
+__device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int col, int c0, int cw) {
+  e.col = col;
   e.A = f.A; e.B = f.B; e.E = f.E;
   e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
+  // slice iz overlaps row r only if iz lies in the open interval
+  // ((r - .5 - E - A)/B, (r + .5 + E - A)/B) of length 1/B + 1; the 0.01 /
+  // 0.02 margins absorb fp32 rounding of lo/hi and of the interval ends
+  const float invB = 1.0f / f.B;
+  e.invB = invB;
+  e.cb = (-0.5f - f.E - f.A) * invB - 0.01f;
+  e.ncand = (int)ceilf((1.0f + 2.0f * f.E) * invB + 0.02f) + 1;
   const Trap p = make_trap(f);
   float ts[FW_CW];
   col_weights<FW_CW>(p, c0, ts);
@@ -327,6 +369,18 @@ __device__ __forceinline__ int block_exclusive_scan(int val, int* warp_tot, int&
   total = warp_tot[FW_WARPS];
   __syncthreads();
   return excl;
+}
+
+// P(r) += sum over NC candidate slices of tt(r, iz) * amp x  (sentinels add 0)
+template <int NC>
+__device__ __forceinline__ float gather_slices(float p, const float4* sb, int i0, float rlo,
+                                               float rhi) {
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const float4 d = sb[i0 + i];
+    p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
+  }
+  return p;
 }
 
 // boundary ray of the tile edge at column coordinate S (centred grid-index coords)
@@ -405,7 +459,7 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
   const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
   const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
 
-  int* prefix = reinterpret_cast<int*>(sbuf + FW_WARPS * FW_VBUF);  // nP + 1
+  int* prefix = reinterpret_cast<int*>(sbuf + FW_WARPS * FW_SBUF);  // nP + 1
   int* jlo = prefix + (nP + 1);                                     // nP
   int* scan_tmp = jlo + nP + 1;                                     // FW_WARPS + 1
   const int seg = (nP + FW_THREADS - 1) / FW_THREADS;
@@ -456,7 +510,9 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
   const float band_hi = (float)min(R0 + FW_ROWS, gp.nr) - 0.5f;
   const size_t ncolvox = (size_t)gp.nx * gp.ny;
   const float* xb = xT + (size_t)b * ncolvox * gp.nz;
-  float4* sw = sbuf + warp * FW_VBUF;
+  float4* sw = sbuf + warp * FW_SBUF;
+  if (lane < FW_PAD) sw[lane] = make_float4(-3e38f, -3e38f, 0.0f, 0.0f);  // lower sentinels
+  const float rw0f = (float)rw0, rw1f = (float)rw1;
 
   for (int base = 0; base < total; base += FW_BATCH) {
     // 2a. one candidate per thread -> footprint setup -> compacted entries
@@ -478,52 +534,62 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
     }
     int nent;
     const int off = block_exclusive_scan(__popc(mask), scan_tmp, nent);
-    if (mask & 1) write_entry(ent[off], f0, ix, iy, c0, cw);
-    if (mask & 2) write_entry(ent[off + (mask & 1)], f1, ix, iy, c0, cw);
+    if (mask & 1) write_entry(ent[off], f0, iy * gp.nx + ix, c0, cw);
+    if (mask & 2) write_entry(ent[off + (mask & 1)], f1, iy * gp.nx + ix, c0, cw);
     __syncthreads();
 
     // 2b. every warp gathers every entry into its own rows
     if (rw0 <= rw1) {
       for (int e = 0; e < nent; ++e) {
         const FwEntry& E = ent[e];
-        const float A = E.A, B = E.B, Eh = E.E;
-        const float invB = __fdividef(1.0f, B);
-        // slices whose axial interval can reach rows [rw0, rw1]
-        int za = (int)floorf(((float)rw0 - 0.5f - Eh - A) * invB) - 1;
-        int zb = (int)ceilf(((float)rw1 + 0.5f + Eh - A) * invB) + 1;
-        za = max(za, 0);
-        zb = min(zb, gp.nz - 1);
+        const float A = E.A, B = E.B, Eh = E.E, invB = E.invB, cb = E.cb;
+        const int nc = E.ncand;
+        // slices that can reach rows [rw0, rw1]
+        const int za = max((int)floorf(fmaf(rw0f, invB, cb)) + 1, 0);
+        const int zb = min((int)floorf(fmaf(rw1f, invB, cb)) + nc, gp.nz - 1);
         if (za > zb) continue;
-        const int NC = (int)ceilf((1.0f + 2.0f * Eh) * invB) + 2;
-        const float zbase = (-0.5f - Eh - A) * invB;
-        const int col = (E.ixy >> 16) * gp.nx + (E.ixy & 0xffff);
-        const float* xc = xb + (size_t)col * gp.nz;
+        const float* xc = xb + (size_t)E.col * gp.nz;
         const float lxy = E.lxy, a0 = E.a0, a1 = E.a1;
         float P[FW_KR];
 #pragma unroll
         for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
         for (int piece = za; piece <= zb; piece += FW_VBUF) {
           const int pe = min(piece + FW_VBUF - 1, zb);
-          for (int iz = piece + lane; iz <= pe; iz += 32) {
-            const float T = fma_(B, (float)iz, A);
-            const float q = fma_(a1, (float)iz, a0);
+          const int nvox = pe - piece + 1;
+          for (int i = lane; i < nvox; i += 32) {
+            const int iz = piece + i;
+            const float izf = (float)iz;
+            const float T = fma_(B, izf, A);
+            const float q = fma_(a1, izf, a0);
             const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-            sw[iz - piece] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + iz)), 0.0f);
+            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + iz)), 0.0f);
           }
+          if (lane < FW_PAD) sw[FW_PAD + nvox + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
           __syncwarp();
+          const int lim = FW_PAD + nvox;  // candidates start in [0, lim]
 #pragma unroll
           for (int kk = 0; kk < FW_KR; ++kk) {
             const int r = rw0 + 32 * kk + lane;
-            if (r > rw1) continue;
             const float rf = (float)r;
+            const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
+            const int i0 = min(max(c, 0), lim);
             const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
-            const int cz = (int)floorf(fmaf(rf, invB, zbase)) - 1;
-            const int i0 = max(cz, piece), i1 = min(cz + NC - 1, pe);
             float p = P[kk];
-            for (int i = i0; i <= i1; ++i) {
-              const float4 d = sw[i - piece];
-              const float tt = sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y));
-              p = fma_(tt, d.z, p);
+            if (nc <= FW_PAD) {
+              switch (nc) {
+                case 1: p = gather_slices<1>(p, sw, i0, rlo, rhi); break;
+                case 2: p = gather_slices<2>(p, sw, i0, rlo, rhi); break;
+                case 3: p = gather_slices<3>(p, sw, i0, rlo, rhi); break;
+                case 4: p = gather_slices<4>(p, sw, i0, rlo, rhi); break;
+                case 5: p = gather_slices<5>(p, sw, i0, rlo, rhi); break;
+                default: p = gather_slices<6>(p, sw, i0, rlo, rhi); break;
+              }
+            } else {  // tiny slices (B < ~0.25): walk the candidates, staying in the piece
+              const int j1 = min(c + nc - 1, lim - 1);
+              for (int j = max(c, FW_PAD); j <= j1; ++j) {
+                const float4 d = sw[j];
+                p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
+              }
             }
             P[kk] = p;
           }
