@@ -30,7 +30,7 @@
 #include "sf_launch.h"
 
 #ifndef CTP_BK_MINB
-#define CTP_BK_MINB 3  // resident CTAs/SM the back kernel is register-budgeted for
+#define CTP_BK_MINB 4  // resident CTAs/SM the back kernel is register-budgeted for
 #endif
 #ifndef CTP_FW_MINB
 #define CTP_FW_MINB 3
@@ -341,7 +341,7 @@ __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int co
     const int cc = c0 + c;
     e.ts[c] = (cc >= lo && cc <= hi) ? ts[c] : 0.0f;
   }
-  e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);
+  e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);  // informational
 }
 
 // exclusive scan of one int per thread over the CTA; returns the total
@@ -406,24 +406,20 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
   }
 }
 
-// y(r, c) += ts(c) * P(r) for the tile columns an entry reaches
-__device__ __forceinline__ void apply_cols(float (&acc)[FW_CW], const FwEntry& E, float P) {
-  const int off = E.cinfo & 0xff, n = E.cinfo >> 8;
-  if (n <= 3) {
-    switch (off) {
-#define CTP_CASE(o)                                                          \
-  case o:                                                                    \
-    acc[o] = fma_(E.ts[o], P, acc[o]);                                       \
-    if (o + 1 < FW_CW) acc[(o + 1) % FW_CW] = fma_(E.ts[(o + 1) % FW_CW], P, acc[(o + 1) % FW_CW]); \
-    if (o + 2 < FW_CW) acc[(o + 2) % FW_CW] = fma_(E.ts[(o + 2) % FW_CW], P, acc[(o + 2) % FW_CW]); \
-    break;
-      CTP_CASE(0) CTP_CASE(1) CTP_CASE(2) CTP_CASE(3) CTP_CASE(4) CTP_CASE(5) CTP_CASE(6) CTP_CASE(7)
-#undef CTP_CASE
-      default: break;
-    }
-  } else {
+// rows of one 32-row group: P(r) = sum over NC candidate slices; then
+// y(r, c) += ts(c) P(r) for all tile columns (ts = 0 where the footprint ends)
+template <int NC>
+__device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
+                                        const float4* sw, int rw0, int lane, float invB, float cb,
+                                        int base, int lim) {
 #pragma unroll
-    for (int c = 0; c < FW_CW; ++c) acc[c] = fma_(E.ts[c], P, acc[c]);
+  for (int kk = 0; kk < FW_KR; ++kk) {
+    const float rf = (float)(rw0 + 32 * kk + lane);
+    const int c = (int)floorf(fmaf(rf, invB, cb)) + base;
+    const int i0 = min(max(c, 0), lim);
+    const float p = gather_slices<NC>(0.0f, sw, i0, sub_(rf, 0.5f), add_(rf, 0.5f));
+#pragma unroll
+    for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], p, acc[kk][cc]);
   }
 }
 
@@ -542,14 +538,39 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
     if (rw0 <= rw1) {
       for (int e = 0; e < nent; ++e) {
         const FwEntry& E = ent[e];
-        const float A = E.A, B = E.B, Eh = E.E, invB = E.invB, cb = E.cb;
+        const float invB = E.invB, cb = E.cb;
         const int nc = E.ncand;
         // slices that can reach rows [rw0, rw1]
         const int za = max((int)floorf(fmaf(rw0f, invB, cb)) + 1, 0);
         const int zb = min((int)floorf(fmaf(rw1f, invB, cb)) + nc, gp.nz - 1);
         if (za > zb) continue;
+        const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
         const float* xc = xb + (size_t)E.col * gp.nz;
-        const float lxy = E.lxy, a0 = E.a0, a1 = E.a1;
+        float ts[FW_CW];
+#pragma unroll
+        for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
+        const int nvox_all = zb - za + 1;
+        if (nvox_all <= FW_VBUF && nc <= 6) {
+          // single piece: stage (lo, hi, amp*x) of slices za..zb between zero sentinels
+#pragma unroll 2
+          for (int i = lane; i < nvox_all; i += 32) {
+            const float izf = (float)(za + i);
+            const float T = fma_(B, izf, A);
+            const float q = fma_(a1, izf, a0);
+            const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
+            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + za + i)), 0.0f);
+          }
+          if (lane < FW_PAD) sw[FW_PAD + nvox_all + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
+          __syncwarp();
+          const int base = 1 - za + FW_PAD, lim = FW_PAD + nvox_all;
+          if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+          else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+          else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+          else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+          __syncwarp();
+          continue;
+        }
+        // generic: several pieces and/or many candidates per row
         float P[FW_KR];
 #pragma unroll
         for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
@@ -557,46 +578,33 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
           const int pe = min(piece + FW_VBUF - 1, zb);
           const int nvox = pe - piece + 1;
           for (int i = lane; i < nvox; i += 32) {
-            const int iz = piece + i;
-            const float izf = (float)iz;
+            const float izf = (float)(piece + i);
             const float T = fma_(B, izf, A);
             const float q = fma_(a1, izf, a0);
             const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + iz)), 0.0f);
+            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + piece + i)), 0.0f);
           }
           if (lane < FW_PAD) sw[FW_PAD + nvox + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
           __syncwarp();
-          const int lim = FW_PAD + nvox;  // candidates start in [0, lim]
 #pragma unroll
           for (int kk = 0; kk < FW_KR; ++kk) {
-            const int r = rw0 + 32 * kk + lane;
-            const float rf = (float)r;
-            const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
-            const int i0 = min(max(c, 0), lim);
+            const float rf = (float)(rw0 + 32 * kk + lane);
             const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
+            const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
+            const int j1 = min(c + nc - 1, FW_PAD + nvox - 1);
             float p = P[kk];
-            if (nc <= FW_PAD) {
-              switch (nc) {
-                case 1: p = gather_slices<1>(p, sw, i0, rlo, rhi); break;
-                case 2: p = gather_slices<2>(p, sw, i0, rlo, rhi); break;
-                case 3: p = gather_slices<3>(p, sw, i0, rlo, rhi); break;
-                case 4: p = gather_slices<4>(p, sw, i0, rlo, rhi); break;
-                case 5: p = gather_slices<5>(p, sw, i0, rlo, rhi); break;
-                default: p = gather_slices<6>(p, sw, i0, rlo, rhi); break;
-              }
-            } else {  // tiny slices (B < ~0.25): walk the candidates, staying in the piece
-              const int j1 = min(c + nc - 1, lim - 1);
-              for (int j = max(c, FW_PAD); j <= j1; ++j) {
-                const float4 d = sw[j];
-                p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
-              }
+            for (int j = max(c, FW_PAD); j <= j1; ++j) {
+              const float4 d = sw[j];
+              p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
             }
             P[kk] = p;
           }
           __syncwarp();
         }
 #pragma unroll
-        for (int kk = 0; kk < FW_KR; ++kk) apply_cols(acc[kk], E, P[kk]);
+        for (int kk = 0; kk < FW_KR; ++kk)
+#pragma unroll
+          for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], P[kk], acc[kk][cc]);
       }
     }
     __syncthreads();  // entries are overwritten by the next round
