@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           const float t1 = e.ncol > 1 ? e.ts[1] : 0.0f;
           const float t2 = e.ncol > 2 ? e.ts[2] : 0.0f;
           const float t3 = e.ncol > 3 ? e.ts[3] : 0.0f;
+#pragma unroll 4
           for (int t = lane; t < nq; t += 32) {
             const int r = Ra + t;
             const bool in = (unsigned)r < (unsigned)nr;
@@ -286,14 +287,14 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 // ---------------------------------------------------------------------------
 // forward projection: y = A x
 // ---------------------------------------------------------------------------
-constexpr int FW_WARPS = 8;
-constexpr int FW_THREADS = FW_WARPS * 32;
 constexpr int FW_CW = 8;                        // detector columns per tile
-constexpr int FW_KR = 3;                        // 32-row groups per warp
-constexpr int FW_ROWS = FW_WARPS * 32 * FW_KR;  // rows per tile
-constexpr int FW_BATCH = FW_THREADS;            // candidate columns per setup round
+#ifndef CTP_FW_KR
+#define CTP_FW_KR 6
+#endif
+constexpr int FW_KR = CTP_FW_KR;                // 32-row groups per warp
+constexpr int FW_ROWS = 32 * FW_KR;             // rows per warp task
 constexpr int FW_PAD = 6;                       // zero sentinels on each side of a piece
-constexpr int FW_VBUF = 192;                    // slices staged per warp and piece
+constexpr int FW_VBUF = 32 * FW_KR + 96;        // slices staged per warp and piece
 constexpr int FW_SBUF = FW_VBUF + 2 * FW_PAD;
 
 struct FwEntry {
@@ -308,10 +309,6 @@ struct FwEntry {
 };
 static_assert(sizeof(FwEntry) == 80, "FwEntry layout");
 
-size_t forward_smem_bytes(int n_primary) {
-  return sizeof(FwEntry) * 2 * FW_BATCH + sizeof(float4) * FW_WARPS * FW_SBUF +
-         sizeof(int) * (2 * (size_t)n_primary + 2) + sizeof(int) * 2 * (FW_WARPS + 1);
-}
 
 __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams& gp, int c0, int cw,
                                              float band_lo, float band_hi) {
@@ -342,33 +339,6 @@ __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int co
     e.ts[c] = (cc >= lo && cc <= hi) ? ts[c] : 0.0f;
   }
   e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);  // informational
-}
-
-// exclusive scan of one int per thread over the CTA; returns the total
-__device__ __forceinline__ int block_exclusive_scan(int val, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int inc = val;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int n = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc += n;
-  }
-  if (lane == 31) warp_tot[warp] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int w = 0; w < FW_WARPS; ++w) {
-      const int t = warp_tot[w];
-      warp_tot[w] = run;
-      run += t;
-    }
-    warp_tot[FW_WARPS] = run;
-  }
-  __syncthreads();
-  const int excl = warp_tot[warp] + inc - val;
-  total = warp_tot[FW_WARPS];
-  __syncthreads();
-  return excl;
 }
 
 // P(r) += sum over NC candidate slices of tt(r, iz) * amp x  (sentinels add 0)
@@ -423,24 +393,169 @@ __device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float 
   }
 }
 
-__global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(GridParams gp,
-                                                                const ViewCoef* __restrict__ vcoef,
-                                                                const float* __restrict__ xT,
-                                                                float* __restrict__ y,
-                                                                int accumulate, int view_batch0) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FwEntry* ent = reinterpret_cast<FwEntry*>(smem_raw);
-  float4* sbuf = reinterpret_cast<float4*>(ent + 2 * FW_BATCH);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// ---- warp-independent forward ------------------------------------------------
+// One WARP owns one task = (view, FW_CW-column tile, FW_KR*32-row band).  It
+// enumerates the wedge of voxel columns reaching its tile (rows of primary
+// indices in chunks of 32, counts prefix-scanned with shuffles), sets the
+// candidates up lane-parallel (one per lane), compacts the surviving
+// (sub-)footprints into its private entry buffer, and gathers them into its
+// register tile.  No CTA barriers: warps of a CTA never wait for each other.
+constexpr int FV_WARPS = 4;
+constexpr int FV_EBUF = 96;  // >= 31 pending + 64 from one setup round
 
-  const int vb = blockIdx.z + view_batch0;
+struct FvSmem {
+  FwEntry ent[FV_EBUF];
+  float4 sbuf[FW_SBUF];
+};
+
+size_t forward_warp_smem_bytes() { return sizeof(FvSmem) * FV_WARPS; }
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += n;
+  }
+  return v;
+}
+
+// slice range of entry E that can reach rows [rw0, rw1]
+__device__ __forceinline__ void fw_range(const FwEntry& E, float rw0f, float rw1f, int nz, int& za,
+                                         int& zb) {
+  za = max((int)floorf(fmaf(rw0f, E.invB, E.cb)) + 1, 0);
+  zb = min((int)floorf(fmaf(rw1f, E.invB, E.cb)) + E.ncand, nz - 1);
+}
+
+constexpr int FW_NPF = (FW_VBUF + 31) / 32;  // prefetched x values per lane
+
+// issue the loads of x for slices za.. (at most FW_VBUF) of one voxel column
+__device__ __forceinline__ void fw_prefetch(float (&xr)[FW_NPF], const float* __restrict__ xc, int za,
+                                            int nvox, int lane) {
+#pragma unroll
+  for (int t = 0; t < FW_NPF; ++t) {
+    const int i = lane + 32 * t;
+    xr[t] = i < nvox ? __ldg(xc + za + i) : 0.0f;
+  }
+}
+
+__device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_KR][FW_CW],
+                                           const GridParams& gp, const float* __restrict__ xb,
+                                           int rw0, int rw1, int lane) {
+  float4* sw = S.sbuf;
+  const float rw0f = (float)rw0, rw1f = (float)rw1;
+  // software pipeline: x of the next fast-path entry is in flight while the
+  // current entry is gathered
+  float xr[FW_NPF];
+  int e_pf = 0;  // entry whose x is in xr (or nent if none)
+  auto next_fast = [&](int e) {
+    for (; e < nent; ++e) {
+      int za, zb;
+      fw_range(S.ent[e], rw0f, rw1f, gp.nz, za, zb);
+      if (za <= zb && zb - za + 1 <= FW_VBUF && S.ent[e].ncand <= 6) {
+        fw_prefetch(xr, xb + (size_t)S.ent[e].col * gp.nz, za, zb - za + 1, lane);
+        return e;
+      }
+    }
+    return nent;
+  };
+  e_pf = next_fast(0);
+  for (int e = 0; e < nent; ++e) {
+    const FwEntry& E = S.ent[e];
+    const float invB = E.invB, cb = E.cb;
+    const int nc = E.ncand;
+    int za, zb;
+    fw_range(E, rw0f, rw1f, gp.nz, za, zb);
+    if (za > zb) continue;
+    const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
+    const float* xc = xb + (size_t)E.col * gp.nz;
+    float ts[FW_CW];
+#pragma unroll
+    for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
+    const int nvox_all = zb - za + 1;
+    if (e == e_pf) {
+      // stage (lo, hi, amp*x) of slices za..zb between zero sentinels
+#pragma unroll
+      for (int t = 0; t < FW_NPF; ++t) {
+        const int i = lane + 32 * t;
+        if (i < nvox_all) {
+          const float izf = (float)(za + i);
+          const float T = fma_(B, izf, A);
+          const float q = fma_(a1, izf, a0);
+          const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
+          sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, xr[t]), 0.0f);
+        }
+      }
+      if (lane < FW_PAD) sw[FW_PAD + nvox_all + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
+      __syncwarp();
+      e_pf = next_fast(e + 1);  // loads for the next entry overlap this gather
+      const int base = 1 - za + FW_PAD, lim = FW_PAD + nvox_all;
+      if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+      else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+      else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+      else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+      __syncwarp();
+      continue;
+    }
+    // generic: several pieces and/or many candidates per row
+    float P[FW_KR];
+#pragma unroll
+    for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
+    for (int piece = za; piece <= zb; piece += FW_VBUF) {
+      const int pe = min(piece + FW_VBUF - 1, zb);
+      const int nvox = pe - piece + 1;
+      for (int i = lane; i < nvox; i += 32) {
+        const float izf = (float)(piece + i);
+        const float T = fma_(B, izf, A);
+        const float q = fma_(a1, izf, a0);
+        const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
+        sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + piece + i)), 0.0f);
+      }
+      if (lane < FW_PAD) sw[FW_PAD + nvox + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
+      __syncwarp();
+#pragma unroll
+      for (int kk = 0; kk < FW_KR; ++kk) {
+        const float rf = (float)(rw0 + 32 * kk + lane);
+        const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
+        const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
+        const int j1 = min(c + nc - 1, FW_PAD + nvox - 1);
+        float p = P[kk];
+        for (int j = max(c, FW_PAD); j <= j1; ++j) {
+          const float4 d = sw[j];
+          p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
+        }
+        P[kk] = p;
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int kk = 0; kk < FW_KR; ++kk)
+#pragma unroll
+      for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], P[kk], acc[kk][cc]);
+  }
+}
+
+__global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
+    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xT,
+    float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  FvSmem& S = reinterpret_cast<FvSmem*>(smem_raw)[warp];
+  const long long task = task0 + (long long)blockIdx.x * FV_WARPS + warp;
+  if (task >= ntasks) return;  // warp-uniform; no CTA barriers in this kernel
+  const int nbands = (gp.nr + FW_ROWS - 1) / FW_ROWS;
+  const int ntiles = (gp.nc + FW_CW - 1) / FW_CW;
+  const int band = (int)(task % nbands);
+  const long long t2 = task / nbands;
+  const int tile = (int)(t2 % ntiles);
+  const int vb = (int)(t2 / ntiles);
   const int v = vb % gp.nv, b = vb / gp.nv;
-  const int c0 = blockIdx.x * FW_CW;
+  const int c0 = tile * FW_CW;
   const int cw = min(FW_CW, gp.nc - c0);
-  const int R0 = blockIdx.y * FW_ROWS;
+  const int rw0 = band * FW_ROWS;
+  const int rw1 = min(rw0 + FW_ROWS, gp.nr) - 1;
   const ViewCoef vc = vcoef[v];
 
-  // ---- 1. strip of candidate voxel columns (wedge between the tile's edge rays)
+  // wedge between the tile's edge rays, in (primary, secondary) grid axes
   float plx, ply, dlx, dly, phx, phy, dhx, dhy;
   edge_ray(vc, gp, (float)c0 - 0.5f, plx, ply, dlx, dly);
   edge_ray(vc, gp, (float)(c0 + cw) - 0.5f, phx, phy, dhx, dhy);
@@ -454,163 +569,77 @@ __global__ void __launch_bounds__(FW_THREADS, CTP_FW_MINB) sf_forward_kernel(Gri
   const float hdp = primary_x ? dhx : dhy, hdq = primary_x ? dhy : dhx;
   const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
   const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
+  const float band_lo = (float)rw0 - 0.5f, band_hi = (float)rw1 + 0.5f;
 
-  int* prefix = reinterpret_cast<int*>(sbuf + FW_WARPS * FW_SBUF);  // nP + 1
-  int* jlo = prefix + (nP + 1);                                     // nP
-  int* scan_tmp = jlo + nP + 1;                                     // FW_WARPS + 1
-  const int seg = (nP + FW_THREADS - 1) / FW_THREADS;
-  int my_sum = 0;
-  for (int t = 0; t < seg; ++t) {
-    const int i = tid * seg + t;
-    if (i >= nP) break;
-    int jl = 0, jh = nQ - 1;
-    if (cull) {
-      const float pa = (float)i - halfP, pb = pa + 1.0f;
-      const float q0 = lq + (pa - lp) * lslope, q1 = lq + (pb - lp) * lslope;
-      const float q2 = hq + (pa - hp) * hslope, q3 = hq + (pb - hp) * hslope;
-      const float qmin = fminf(fminf(q0, q1), fminf(q2, q3)) + halfQ;
-      const float qmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) + halfQ;
-      if (qmin > -1e8f && qmax < 1e8f) {
-        jl = max(jl, (int)floorf(qmin) - 1);
-        jh = min(jh, (int)floorf(qmax) + 1);
-      }
-    }
-    const int n = jh >= jl ? jh - jl + 1 : 0;
-    jlo[i] = jl;
-    prefix[i] = n;  // counts for now
-    my_sum += n;
-  }
-  __syncthreads();
-  int total;
-  int run = block_exclusive_scan(my_sum, scan_tmp, total);
-  for (int t = 0; t < seg; ++t) {
-    const int i = tid * seg + t;
-    if (i >= nP) break;
-    const int n = prefix[i];
-    prefix[i] = run;
-    run += n;
-  }
-  if (tid == 0) prefix[nP] = total;
-  __syncthreads();
-
-  // ---- 2. accumulate the tile
   float acc[FW_KR][FW_CW];
 #pragma unroll
   for (int k = 0; k < FW_KR; ++k)
 #pragma unroll
     for (int c = 0; c < FW_CW; ++c) acc[k][c] = 0.0f;
+  if (lane < FW_PAD) S.sbuf[lane] = make_float4(-3e38f, -3e38f, 0.0f, 0.0f);  // lower sentinels
+  const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
 
-  const int rw0 = R0 + warp * 32 * FW_KR;
-  const int rw1 = min(rw0 + 32 * FW_KR, gp.nr) - 1;  // last row of this warp
-  const float band_lo = (float)R0 - 0.5f;
-  const float band_hi = (float)min(R0 + FW_ROWS, gp.nr) - 0.5f;
-  const size_t ncolvox = (size_t)gp.nx * gp.ny;
-  const float* xb = xT + (size_t)b * ncolvox * gp.nz;
-  float4* sw = sbuf + warp * FW_SBUF;
-  if (lane < FW_PAD) sw[lane] = make_float4(-3e38f, -3e38f, 0.0f, 0.0f);  // lower sentinels
-  const float rw0f = (float)rw0, rw1f = (float)rw1;
-
-  for (int base = 0; base < total; base += FW_BATCH) {
-    // 2a. one candidate per thread -> footprint setup -> compacted entries
-    const int k = base + tid;
-    SubFoot f0, f1;
-    int mask = 0, ix = 0, iy = 0;
-    if (k < total) {
-      int lo = 0, hi = nP;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (prefix[mid] <= k) lo = mid; else hi = mid;
+  int pending = 0;
+  for (int ib = 0; ib < nP; ib += 32) {
+    // secondary-index range of primary index i on the two edge rays (+-1 margin)
+    const int i = ib + lane;
+    int jl = 0, cnt = 0;
+    if (i < nP) {
+      int jh = nQ - 1;
+      if (cull) {
+        const float pa = (float)i - halfP, pb = pa + 1.0f;
+        const float q0 = lq + (pa - lp) * lslope, q1 = lq + (pb - lp) * lslope;
+        const float q2 = hq + (pa - hp) * hslope, q3 = hq + (pb - hp) * hslope;
+        const float qmin = fminf(fminf(q0, q1), fminf(q2, q3)) + halfQ;
+        const float qmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) + halfQ;
+        if (qmin > -1e8f && qmax < 1e8f) {
+          jl = max(jl, (int)floorf(qmin) - 1);
+          jh = min(jh, (int)floorf(qmax) + 1);
+        }
       }
-      const int i = lo, j = jlo[i] + (k - prefix[i]);
-      ix = primary_x ? i : j;
-      iy = primary_x ? j : i;
-      mask = column_footprint(vc, gp, ix, iy, f0, f1);
-      if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
-      if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
+      cnt = jh >= jl ? jh - jl + 1 : 0;
     }
-    int nent;
-    const int off = block_exclusive_scan(__popc(mask), scan_tmp, nent);
-    if (mask & 1) write_entry(ent[off], f0, iy * gp.nx + ix, c0, cw);
-    if (mask & 2) write_entry(ent[off + (mask & 1)], f1, iy * gp.nx + ix, c0, cw);
-    __syncthreads();
-
-    // 2b. every warp gathers every entry into its own rows
-    if (rw0 <= rw1) {
-      for (int e = 0; e < nent; ++e) {
-        const FwEntry& E = ent[e];
-        const float invB = E.invB, cb = E.cb;
-        const int nc = E.ncand;
-        // slices that can reach rows [rw0, rw1]
-        const int za = max((int)floorf(fmaf(rw0f, invB, cb)) + 1, 0);
-        const int zb = min((int)floorf(fmaf(rw1f, invB, cb)) + nc, gp.nz - 1);
-        if (za > zb) continue;
-        const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
-        const float* xc = xb + (size_t)E.col * gp.nz;
-        float ts[FW_CW];
+    const int incl = warp_incl_scan(cnt, lane);
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int cbase = 0; cbase < total; cbase += 32) {
+      const int k = cbase + lane;
+      // owner lane o: the largest lane with excl_o <= k (it has cnt_o > 0)
+      int o = 0;
 #pragma unroll
-        for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
-        const int nvox_all = zb - za + 1;
-        if (nvox_all <= FW_VBUF && nc <= 6) {
-          // single piece: stage (lo, hi, amp*x) of slices za..zb between zero sentinels
-#pragma unroll 2
-          for (int i = lane; i < nvox_all; i += 32) {
-            const float izf = (float)(za + i);
-            const float T = fma_(B, izf, A);
-            const float q = fma_(a1, izf, a0);
-            const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + za + i)), 0.0f);
-          }
-          if (lane < FW_PAD) sw[FW_PAD + nvox_all + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
-          __syncwarp();
-          const int base = 1 - za + FW_PAD, lim = FW_PAD + nvox_all;
-          if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-          else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-          else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-          else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-          __syncwarp();
-          continue;
-        }
-        // generic: several pieces and/or many candidates per row
-        float P[FW_KR];
-#pragma unroll
-        for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
-        for (int piece = za; piece <= zb; piece += FW_VBUF) {
-          const int pe = min(piece + FW_VBUF - 1, zb);
-          const int nvox = pe - piece + 1;
-          for (int i = lane; i < nvox; i += 32) {
-            const float izf = (float)(piece + i);
-            const float T = fma_(B, izf, A);
-            const float q = fma_(a1, izf, a0);
-            const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-            sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + piece + i)), 0.0f);
-          }
-          if (lane < FW_PAD) sw[FW_PAD + nvox + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
-          __syncwarp();
-#pragma unroll
-          for (int kk = 0; kk < FW_KR; ++kk) {
-            const float rf = (float)(rw0 + 32 * kk + lane);
-            const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
-            const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
-            const int j1 = min(c + nc - 1, FW_PAD + nvox - 1);
-            float p = P[kk];
-            for (int j = max(c, FW_PAD); j <= j1; ++j) {
-              const float4 d = sw[j];
-              p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
-            }
-            P[kk] = p;
-          }
-          __syncwarp();
-        }
-#pragma unroll
-        for (int kk = 0; kk < FW_KR; ++kk)
-#pragma unroll
-          for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], P[kk], acc[kk][cc]);
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, excl, o + step);
+        if (ex <= k) o += step;
+      }
+      const int jo = __shfl_sync(0xffffffffu, jl, o);
+      const int exo = __shfl_sync(0xffffffffu, excl, o);
+      SubFoot f0, f1;
+      int mask = 0, col = 0;
+      if (k < total) {
+        const int ii = ib + o, j = jo + (k - exo);
+        const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
+        col = iy * gp.nx + ix;
+        mask = column_footprint(vc, gp, ix, iy, f0, f1);
+        if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
+        if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
+      }
+      const int n = __popc(mask);
+      const int ni = warp_incl_scan(n, lane);
+      const int off = pending + ni - n;
+      if (mask & 1) write_entry(S.ent[off], f0, col, c0, cw);
+      if (mask & 2) write_entry(S.ent[off + (mask & 1)], f1, col, c0, cw);
+      pending += __shfl_sync(0xffffffffu, ni, 31);
+      __syncwarp();
+      if (pending >= 32) {
+        fw_process(S, pending, acc, gp, xb, rw0, rw1, lane);
+        pending = 0;
+        __syncwarp();
       }
     }
-    __syncthreads();  // entries are overwritten by the next round
   }
+  if (pending > 0) fw_process(S, pending, acc, gp, xb, rw0, rw1, lane);
 
-  // ---- 3. store the tile: y[b][v][r][c0 + c]
+  // store the tile: y[b][v][r][c0 + c]
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
 #pragma unroll
   for (int kk = 0; kk < FW_KR; ++kk) {
@@ -655,16 +684,20 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float
 
 cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const float* xT, float* sino,
                            int batch, bool accumulate, cudaStream_t st) {
-  const int nP = gp.nx > gp.ny ? gp.nx : gp.ny;
-  const size_t smem = forward_smem_bytes(nP);
+  const size_t smem = forward_warp_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(sf_forward_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int total = gp.nv * batch;
-  for (int z0 = 0; z0 < total; z0 += 65535) {
-    const int nz = min(65535, total - z0);
-    const dim3 grid((gp.nc + FW_CW - 1) / FW_CW, (gp.nr + FW_ROWS - 1) / FW_ROWS, nz);
-    sf_forward_kernel<<<grid, FW_THREADS, smem, st>>>(gp, vcoef, xT, sino, accumulate ? 1 : 0, z0);
+  const long long nbands = (gp.nr + FW_ROWS - 1) / FW_ROWS;
+  const long long ntiles = (gp.nc + FW_CW - 1) / FW_CW;
+  const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
+  const long long max_blocks = 1LL << 30;
+  for (long long t0 = 0; t0 < ntasks; t0 += max_blocks * FV_WARPS) {
+    const long long rem = ntasks - t0;
+    const long long nb = (rem + FV_WARPS - 1) / FV_WARPS;
+    const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
+    sf_forward_kernel<<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xT, sino, accumulate ? 1 : 0, t0,
+                                                         ntasks);
   }
   return cudaGetLastError();
 }

@@ -18,6 +18,6 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
 // yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
                         int batch, bool accumulate, cudaStream_t st);
-size_t forward_smem_bytes(int n_primary);
+size_t forward_warp_smem_bytes();
 
 }  // namespace ctp
