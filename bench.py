@@ -142,7 +142,11 @@ def cpu_sample(cfg: dict, budget_s: float = 20.0):
     y1 = np.random.default_rng(1).random((1,) + tuple(shape_s[1:]), dtype=np.float32)
     oracle.sf_back(one, y1)
     t1 = time.perf_counter() - t0
-    k = int(max(1, min(nv, budget_s / max(t1, 1e-3))))
+    # the reference forward parallelises over views (prange, _kernels.py:655): use a
+    # multiple of the thread count so every core works, as in the full workload
+    k = int(max(1, budget_s * threads / max(t1, 1e-3)))
+    k = max(threads, (k // threads) * threads)
+    k = min(nv, k)
     idx = [int(round(i * nv / k)) % nv for i in range(k)]
     sub = oracle.with_views(cfg, idx)
     y = np.random.default_rng(1).random((k,) + tuple(shape_s[1:]), dtype=np.float32)
@@ -172,7 +176,9 @@ def run_reference(args, cfg):
     nv = shape_s[0]
     nvox = int(np.prod(shape_v))
     x = np.random.default_rng(0).random(shape_v, dtype=np.float32)
-    views_per_step = max(1, int(os.environ.get("BENCH_REF_VIEWS", "1")))
+    # one view per host thread per step: the reference forward parallelises over
+    # views (_kernels.py:655) and the back over voxel columns (_kernels.py:676)
+    views_per_step = max(1, int(os.environ.get("BENCH_REF_VIEWS", str(threads))))
     y = np.random.default_rng(1).random((views_per_step,) + tuple(shape_s[1:]), dtype=np.float32)
     times = []
     for step in range(args.warmup + args.steps):

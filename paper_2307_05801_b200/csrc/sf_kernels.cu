@@ -136,17 +136,56 @@ __device__ __noinline__ float back_voxel_direct(float acc, float amp, float lo, 
   return acc;
 }
 
-// table path: acc += sum_k (amp * tt_k) * Q(r0 + k), K rows, Q from smem
+// Table path for a PAIR of slices (izf.x, izf.y), packed f32x2: each slice
+// adds sum_k (amp * tt_k) * Q(r0 + k) over its K rows.  The boundaries of row
+// r0 + k are fl + 0.5 + k and fl + 1.5 + k (fl = r0 - 1); the lowest one is
+// <= lo and the highest >= hi by construction, so their clamps are exactly lo
+// and hi, and every tt_k equals clamp(r+.5,lo,hi) - clamp(r-.5,lo,hi) as the
+// forward kernel evaluates it.
 template <int K>
-__device__ __forceinline__ float back_voxel_rows(float acc, float amp, float lo, float hi,
+__device__ __forceinline__ float2 back_pair_rows(float2 acc, const BkEntry& e, float2 izf,
                                                  const float* qw, int Ra) {
-  const float fl = row_floor(lo);  // r0 - 1 (integer-valued)
-  const float* q = qw + ((int)fl + 1 - Ra);
-  float g = clampf_(add_(fl, 0.5f), lo, hi);
+  const float2 T = fma2_(bc2_(e.B), izf, bc2_(e.A));
+  const float2 lo = add2_(T, bc2_(-e.E)), hi = add2_(T, bc2_(e.E));
+  const float2 q = fma2_(bc2_(e.a1), izf, bc2_(e.a0));
+  const float2 t = fma2_(q, q, bc2_(1.0f));
+  const float2 amp = mul2_(bc2_(e.lxy), make_float2(sqrt_approx(t.x), sqrt_approx(t.y)));
+  const float2 lm = add2_(lo, bc2_(-0.5f));
+  const float2 fl = make_float2(floorf(lm.x), floorf(lm.y));
+  const float* qa = qw + ((int)fl.x + 1 - Ra);
+  const float* qb = qw + ((int)fl.y + 1 - Ra);
+  float2 g = lo;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const float gn = clampf_(add_(fl, (float)k + 1.5f), lo, hi);
-    acc = fma_(mul_(amp, sub_(gn, g)), q[k], acc);
+    float2 gn;
+    if (k == K - 1) {
+      gn = hi;
+    } else {
+      const float2 bnd = add2_(fl, bc2_((float)k + 1.5f));
+      gn = make_float2(clampf_(bnd.x, lo.x, hi.x), clampf_(bnd.y, lo.y, hi.y));
+    }
+    const float2 c = mul2_(amp, add2_(gn, make_float2(-g.x, -g.y)));
+    acc = fma2_(c, make_float2(qa[k], qb[k]), acc);
+    g = gn;
+  }
+  return acc;
+}
+
+// single slice (tail of an odd count), same operations
+template <int K>
+__device__ __forceinline__ float back_one_rows(float acc, const BkEntry& e, float izf,
+                                               const float* qw, int Ra) {
+  const float T = fma_(e.B, izf, e.A);
+  const float lo = add_(T, -e.E), hi = add_(T, e.E);
+  const float q = fma_(e.a1, izf, e.a0);
+  const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+  const float fl = floorf(add_(lo, -0.5f));
+  const float* qa = qw + ((int)fl + 1 - Ra);
+  float g = lo;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float gn = (k == K - 1) ? hi : clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+    acc = fma_(mul_(amp, add_(gn, -g)), qa[k], acc);
     g = gn;
   }
   return acc;
@@ -156,14 +195,15 @@ template <int K>
 __device__ __forceinline__ void back_slices(float (&acc)[BK_ZPL], const BkEntry& e, float izf0,
                                             int nvalid, const float* qw, int Ra) {
 #pragma unroll
-  for (int m = 0; m < BK_ZPL; ++m) {
-    if (m < nvalid) {
-      const float izf = izf0 + (float)(32 * m);
-      const float T = fma_(e.B, izf, e.A);
-      const float lo = sub_(T, e.E), hi = add_(T, e.E);
-      const float q = fma_(e.a1, izf, e.a0);
-      const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
-      acc[m] = back_voxel_rows<K>(acc[m], amp, lo, hi, qw, Ra);
+  for (int m = 0; m < BK_ZPL; m += 2) {
+    if (m + 1 < nvalid) {
+      const float2 r = back_pair_rows<K>(make_float2(acc[m], acc[m + 1]), e,
+                                         make_float2(izf0 + (float)(32 * m), izf0 + (float)(32 * m + 32)),
+                                         qw, Ra);
+      acc[m] = r.x;
+      acc[m + 1] = r.y;
+    } else if (m < nvalid) {
+      acc[m] = back_one_rows<K>(acc[m], e, izf0 + (float)(32 * m), qw, Ra);
     }
   }
 }
@@ -235,16 +275,33 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           const float t1 = e.ncol > 1 ? e.ts[1] : 0.0f;
           const float t2 = e.ncol > 2 ? e.ts[2] : 0.0f;
           const float t3 = e.ncol > 3 ? e.ts[3] : 0.0f;
+          if (Ra >= 0 && Rz < nr) {
+            // rows r and r + 32 per iteration, packed
+            const float2 T0 = bc2_(t0), T1 = bc2_(t1), T2 = bc2_(t2), T3 = bc2_(t3);
+#pragma unroll 2
+            for (int t = lane; t < nq; t += 64) {
+              const int r = Ra + t;
+              const bool two = t + 32 < nq;
+              const int r2 = two ? r + 32 : r;
+              float2 q = mul2_(T0, make_float2(__ldg(p0 + r), __ldg(p0 + r2)));
+              q = fma2_(T1, make_float2(__ldg(p1 + r), __ldg(p1 + r2)), q);
+              q = fma2_(T2, make_float2(__ldg(p2 + r), __ldg(p2 + r2)), q);
+              q = fma2_(T3, make_float2(__ldg(p3 + r), __ldg(p3 + r2)), q);
+              qw[t] = q.x;
+              if (two) qw[t + 32] = q.y;
+            }
+          } else {
 #pragma unroll 4
-          for (int t = lane; t < nq; t += 32) {
-            const int r = Ra + t;
-            const bool in = (unsigned)r < (unsigned)nr;
-            const int rr = in ? r : 0;
-            float q = fma_(t0, __ldg(p0 + rr), 0.0f);
-            q = fma_(t1, __ldg(p1 + rr), q);
-            q = fma_(t2, __ldg(p2 + rr), q);
-            q = fma_(t3, __ldg(p3 + rr), q);
-            qw[t] = in ? q : 0.0f;
+            for (int t = lane; t < nq; t += 32) {
+              const int r = Ra + t;
+              const bool in = (unsigned)r < (unsigned)nr;
+              const int rr = in ? r : 0;
+              float q = mul_(t0, __ldg(p0 + rr));
+              q = fma_(t1, __ldg(p1 + rr), q);
+              q = fma_(t2, __ldg(p2 + rr), q);
+              q = fma_(t3, __ldg(p3 + rr), q);
+              qw[t] = in ? q : 0.0f;
+            }
           }
           __syncwarp();
           if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Ra);
