@@ -35,6 +35,12 @@
 #ifndef CTP_FW_MINB
 #define CTP_FW_MINB 3
 #endif
+#ifndef CTP_FW_GSKIP
+#define CTP_FW_GSKIP 0  // skip 32-row groups outside a column's row span
+#endif
+#ifndef CTP_FW_APPLY2
+#define CTP_FW_APPLY2 1  // packed f32x2 column apply
+#endif
 
 namespace ctp {
 
@@ -398,16 +404,50 @@ __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int co
   e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);  // informational
 }
 
-// P(r) += sum over NC candidate slices of tt(r, iz) * amp x  (sentinels add 0)
+// P(r) += sum over NC candidate slices of tt(r, iz) * amp x  (sentinels add 0).
+// max(0, min(hi, r+.5) - max(lo, r-.5)) equals clamp(r+.5,lo,hi) -
+// clamp(r-.5,lo,hi) bit for bit (same operands when the intervals overlap,
+// exactly 0 otherwise), one instruction shorter.
 template <int NC>
 __device__ __forceinline__ float gather_slices(float p, const float4* sb, int i0, float rlo,
                                                float rhi) {
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     const float4 d = sb[i0 + i];
-    p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
+    p = fma_(fmaxf(sub_(fminf(rhi, d.y), fmaxf(rlo, d.x)), 0.0f), d.z, p);
   }
   return p;
+}
+
+// rows of the 32-row groups [g0, g1] of this warp: P(r) = sum over NC candidate
+// slices; then y(r, c) += ts(c) P(r) for all tile columns (ts = 0 where the
+// footprint ends), two columns per packed FFMA2
+template <int NC>
+__device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
+                                        const float4* sw, int rw0, int lane, float invB, float cb,
+                                        int base, int lim, int g0, int g1) {
+#pragma unroll
+  for (int kk = 0; kk < FW_KR; ++kk) {
+#if CTP_FW_GSKIP
+    if (kk < g0 || kk > g1) continue;  // warp-uniform
+#endif
+    const float rf = (float)(rw0 + 32 * kk + lane);
+    const int c = (int)floorf(fmaf(rf, invB, cb)) + base;
+    const int i0 = min(max(c, 0), lim);
+    const float p = gather_slices<NC>(0.0f, sw, i0, sub_(rf, 0.5f), add_(rf, 0.5f));
+#if CTP_FW_APPLY2
+    const float2 pp = bc2_(p);
+#pragma unroll
+    for (int cc = 0; cc < FW_CW; cc += 2) {
+      const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), pp, make_float2(acc[kk][cc], acc[kk][cc + 1]));
+      acc[kk][cc] = a.x;
+      acc[kk][cc + 1] = a.y;
+    }
+#else
+#pragma unroll
+    for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], p, acc[kk][cc]);
+#endif
+  }
 }
 
 // boundary ray of the tile edge at column coordinate S (centred grid-index coords)
@@ -430,23 +470,6 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
     dx = vc.wx; dy = vc.wy;
   } else {
     dx = px - vc.xs; dy = py - vc.ys;
-  }
-}
-
-// rows of one 32-row group: P(r) = sum over NC candidate slices; then
-// y(r, c) += ts(c) P(r) for all tile columns (ts = 0 where the footprint ends)
-template <int NC>
-__device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
-                                        const float4* sw, int rw0, int lane, float invB, float cb,
-                                        int base, int lim) {
-#pragma unroll
-  for (int kk = 0; kk < FW_KR; ++kk) {
-    const float rf = (float)(rw0 + 32 * kk + lane);
-    const int c = (int)floorf(fmaf(rf, invB, cb)) + base;
-    const int i0 = min(max(c, 0), lim);
-    const float p = gather_slices<NC>(0.0f, sw, i0, sub_(rf, 0.5f), add_(rf, 0.5f));
-#pragma unroll
-    for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], p, acc[kk][cc]);
   }
 }
 
@@ -546,10 +569,14 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this gather
       const int base = 1 - za + FW_PAD, lim = FW_PAD + nvox_all;
-      if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-      else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-      else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
-      else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim);
+      // 32-row groups touched by the column: rows [T(0) - E, T(nz-1) + E]
+      const float tlo = sub_(fma_(B, 0.0f, A), Eh), thi = add_(fma_(B, (float)(gp.nz - 1), A), Eh);
+      const int g0 = max(0, ((int)floorf(tlo) - 1 - rw0) >> 5);
+      const int g1 = min(FW_KR - 1, ((int)ceilf(thi) + 1 - rw0) >> 5);
+      if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
+      else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
+      else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
+      else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
       __syncwarp();
       continue;
     }
@@ -578,7 +605,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
         float p = P[kk];
         for (int j = max(c, FW_PAD); j <= j1; ++j) {
           const float4 d = sw[j];
-          p = fma_(sub_(clampf_(rhi, d.x, d.y), clampf_(rlo, d.x, d.y)), d.z, p);
+          p = fma_(fmaxf(sub_(fminf(rhi, d.y), fmaxf(rlo, d.x)), 0.0f), d.z, p);
         }
         P[kk] = p;
       }
