@@ -38,6 +38,9 @@
 #ifndef CTP_FW_GSKIP
 #define CTP_FW_GSKIP 0  // skip 32-row groups outside a column's row span
 #endif
+#ifndef CTP_FW_SCATTER
+#define CTP_FW_SCATTER 0  // forward phase 2 as conflict-free row scatter (else gather)
+#endif
 #ifndef CTP_FW_APPLY2
 #define CTP_FW_APPLY2 1  // packed f32x2 column apply
 #endif
@@ -483,9 +486,11 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
 constexpr int FV_WARPS = 4;
 constexpr int FV_EBUF = 96;  // >= 31 pending + 64 from one setup round
 
+constexpr int FW_PADR = 8;  // garbage row slots on each side of the row buffer
 struct FvSmem {
   FwEntry ent[FV_EBUF];
   float4 sbuf[FW_SBUF];
+  float prow[FW_ROWS + 2 * FW_PADR];  // per-row partial sums P(r) of one entry
 };
 
 size_t forward_warp_smem_bytes() { return sizeof(FvSmem) * FV_WARPS; }
@@ -515,6 +520,63 @@ __device__ __forceinline__ void fw_prefetch(float (&xr)[FW_NPF], const float* __
   for (int t = 0; t < FW_NPF; ++t) {
     const int i = lane + 32 * t;
     xr[t] = i < nvox ? __ldg(xc + za + i) : 0.0f;
+  }
+}
+
+// Scatter path of one entry: lanes = slices.  Slice iz adds
+// c_k = tt_k * (amp x) to rows r0+k, k < K, with tt_k evaluated exactly as in
+// the back kernel (first boundary lo, last hi, middle ones clamped).  Targets
+// of one RMW step are distinct: r0 strictly increases with iz when B > 1.001;
+// for 0.5005 < B <= 1.001 (PAIR) two neighbouring slices may share r0, and the
+// follower's coefficient is first added to the leader's (no triples occur).
+// Rows outside the warp's band go to garbage slots that are never read.
+template <int K, bool PAIR>
+__device__ __forceinline__ void fw_scatter(float* prow, const FwEntry& E, const float (&xr)[FW_NPF],
+                                           int za, int nvox, int rw0, int lane) {
+  const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
+  constexpr int LAST = FW_ROWS + 2 * FW_PADR - 1;
+#pragma unroll
+  for (int t = 0; t < FW_NPF; ++t) {
+    if (32 * t >= nvox) break;  // warp-uniform
+    const int i = lane + 32 * t;
+    const bool act = i < nvox;
+    const float izf = (float)(za + i);
+    const float T = fma_(B, izf, A);
+    const float lo = add_(T, -Eh), hi = add_(T, Eh);
+    const float q = fma_(a1, izf, a0);
+    const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
+    const float xa = mul_(amp, xr[t]);
+    const float fl = floorf(add_(lo, -0.5f));
+    const int r0 = (int)fl + 1;
+    float c[K];
+    float g = lo;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float gn = (k == K - 1) ? hi : clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+      c[k] = mul_(add_(gn, -g), xa);
+      g = gn;
+    }
+    bool writer = act;
+    if (PAIR) {
+      const int r0p = __shfl_up_sync(0xffffffffu, r0, 1);
+      const int r0n = __shfl_down_sync(0xffffffffu, r0, 1);
+      const bool actn = __shfl_down_sync(0xffffffffu, act ? 1 : 0, 1) != 0;
+      const bool follower = lane > 0 && r0p == r0;   // leader (lane-1) takes our share
+      const bool leader = lane < 31 && actn && r0n == r0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float cn = __shfl_down_sync(0xffffffffu, c[k], 1);
+        if (leader) c[k] = add_(c[k], cn);
+      }
+      writer = act && !follower;
+    }
+    const int base = writer ? r0 - rw0 + FW_PADR : 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = min(max(base + k, 0), LAST);
+      if (writer) prow[j] = add_(prow[j], c[k]);
+      __syncwarp();
+    }
   }
 }
 
@@ -552,6 +614,37 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
 #pragma unroll
     for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
     const int nvox_all = zb - za + 1;
+    const int K = rows_per_slice(B);
+    int mode = 0;  // 0: gather path
+#if CTP_FW_SCATTER
+    if (B > 1.001f) mode = K == 3 ? 1 : (K == 4 ? 2 : 0);
+    else if (B > 0.5005f) mode = K == 2 ? 3 : (K == 3 ? 4 : 0);
+#endif
+    if (e == e_pf && mode != 0) {
+      switch (mode) {
+        case 1: fw_scatter<3, false>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
+        case 2: fw_scatter<4, false>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
+        case 3: fw_scatter<2, true>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
+        default: fw_scatter<3, true>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
+      }
+      e_pf = next_fast(e + 1);  // loads for the next entry overlap the apply
+      // y(r, c) += ts(c) P(r); reset P
+#pragma unroll
+      for (int kk = 0; kk < FW_KR; ++kk) {
+        float* pr = S.prow + FW_PADR + 32 * kk + lane;
+        const float p = *pr;
+        *pr = 0.0f;
+        const float2 pp = bc2_(p);
+#pragma unroll
+        for (int cc = 0; cc < FW_CW; cc += 2) {
+          const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), pp, make_float2(acc[kk][cc], acc[kk][cc + 1]));
+          acc[kk][cc] = a.x;
+          acc[kk][cc + 1] = a.y;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     if (e == e_pf) {
       // stage (lo, hi, amp*x) of slices za..zb between zero sentinels
 #pragma unroll
@@ -661,6 +754,8 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
 #pragma unroll
     for (int c = 0; c < FW_CW; ++c) acc[k][c] = 0.0f;
   if (lane < FW_PAD) S.sbuf[lane] = make_float4(-3e38f, -3e38f, 0.0f, 0.0f);  // lower sentinels
+  for (int j = lane; j < FW_ROWS + 2 * FW_PADR; j += 32) S.prow[j] = 0.0f;
+  __syncwarp();
   const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
 
   int pending = 0;
