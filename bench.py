@@ -40,6 +40,9 @@ CONFIGS = {
     "c3": dict(geometry="cone", numX=512, numY=512, numZ=512, voxelWidth=0.6667,
                voxelHeight=0.6667, numRows=768, numCols=768, pixelHeight=1.0, pixelWidth=1.0,
                sod=1000.0, sdd=1500.0, numAngles=720, angularRange=360.0),
+    "c2": dict(geometry="cone", numX=512, numY=512, numZ=1, voxelWidth=0.6667,
+               voxelHeight=1.0, numRows=1, numCols=768, pixelHeight=1.0, pixelWidth=1.0,
+               sod=1000.0, sdd=1500.0, numAngles=720, angularRange=360.0),
     "c1": dict(geometry="parallel", numX=128, numY=128, numZ=128, voxelWidth=1.0,
                voxelHeight=1.0, numRows=128, numCols=128, pixelHeight=1.0, pixelWidth=1.0,
                numAngles=180, angularRange=180.0),
@@ -47,8 +50,11 @@ CONFIGS = {
 WORKLOAD_NAME = {
     "c3": "cone-beam flat 512^3 x 720 views, 768^2 det, fwd+back (BASELINE configs[2])",
     "c1": "parallel-beam 128^3 x 180 views, 128^2 det, fwd+back (BASELINE configs[0])",
+    "c2": "fan-beam (cone-flat, 1 row, 1 slice) 512^2 x batch 64 x 720 views, 768 cols (BASELINE configs[1])",
 }
 METRIC = "fwd+back projector GUPS, cone-beam 512³ × 720 views"
+METRICS = {"c3": METRIC, "c1": "fwd+back projector GUPS, parallel-beam 128³ × 180 views",
+           "c2": "fwd+back projector GUPS, fan-beam 512² × batch 64 × 720 views"}
 
 
 def _peaks():
@@ -196,7 +202,7 @@ def run_reference(args, cfg):
               "f64 C restatement of the reference kernels (oracle/sf_oracle.c), OpenMP over "
               "host cores; the reference itself is Python/numba and does not travel to the box")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GUPS",
+        "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": "GUPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * t / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic U[0,1) (PCG64 seeds 0/1)",
@@ -219,6 +225,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch", type=int, default=0, help="batch size (default: 64 for c2, else 1)")
     ap.add_argument("--views", type=int, default=0,
                     help="profiling only: restrict to the first N views (not a bench number)")
     args = ap.parse_args()
@@ -251,22 +258,25 @@ def main():
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(0)
-    x = torch.rand((1,) + spec.shape, device=dev, generator=gen)
+    B = args.batch or (64 if args.config == "c2" else 1)
+    x = torch.rand((B,) + spec.shape, device=dev, generator=gen)
     gen.manual_seed(1 + rank)
-    y = torch.rand((1, nv_local, nr, nc), device=dev, generator=gen)
+    y = torch.rand((B, nv_local, nr, nc), device=dev, generator=gen)
     plan = sharded.shard.plan(local)
-    sino_out = torch.empty((1, nv_local, nr, nc), device=dev)
+    sino_out = torch.empty((B, nv_local, nr, nc), device=dev)
 
     def step(time_kernel=False):
         plan.forward(x, out=sino_out, time_kernel=time_kernel)
         if world == 1:
             vol = plan.back(y, time_kernel=time_kernel)
         else:
-            part = torch.zeros((1, sharded.nz_pad) + spec.shape[1:], device=dev)
-            plan.back(y, out=part[:, : spec.numZ], time_kernel=time_kernel)
-            out = torch.empty((sharded.slab,) + spec.shape[1:], device=dev)
-            dist.reduce_scatter_tensor(out, part[0])
-            vol = out
+            vol = sharded.back(y) if B > 1 else None
+            if B == 1:
+                part = torch.zeros((1, sharded.nz_pad) + spec.shape[1:], device=dev)
+                plan.back(y, out=part[:, : spec.numZ], time_kernel=time_kernel)
+                out = torch.empty((sharded.slab,) + spec.shape[1:], device=dev)
+                dist.reduce_scatter_tensor(out, part[0])
+                vol = out
         return vol
 
     for _ in range(args.warmup):
@@ -298,17 +308,17 @@ def main():
         tt = torch.tensor([t_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    total_updates = 2.0 * nvox * g.numViews * args.steps
+    total_updates = 2.0 * B * nvox * g.numViews * args.steps
     value = total_updates / (t_max / 1e3) / 1e9
 
     # roofline of the dominant kernel: algorithmic bytes per
     # launch = 4 B per voxel-view update + 4 B per output element
     peak, peak_kind = _peaks()
     f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(back_ms)
-    upd = nvox * nv_local
+    upd = B * nvox * nv_local
     kern = {
-        "sf_forward_kernel": {"ms": f_ms, "bytes": 4.0 * upd + 4.0 * nv_local * nr * nc},
-        "sf_back_kernel": {"ms": b_ms, "bytes": 4.0 * upd + 4.0 * nvox},
+        "sf_forward_kernel": {"ms": f_ms, "bytes": 4.0 * upd + 4.0 * B * nv_local * nr * nc},
+        "sf_back_kernel": {"ms": b_ms, "bytes": 4.0 * upd + 4.0 * B * nvox},
     }
     for k in kern.values():
         k["gbs"] = k["bytes"] / (k["ms"] / 1e3) / 1e9
@@ -343,7 +353,7 @@ def main():
             tt = torch.tensor([te], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {"value": 2.0 * nvox * g.numViews * args.e2e_steps / te / 1e9, "unit": "GUPS",
+        e2e = {"value": 2.0 * B * nvox * g.numViews * args.e2e_steps / te / 1e9, "unit": "GUPS",
                "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 4),
                "d2h_bytes_per_step": int(yo.numel() * 4 + xo.numel() * 4),
                "steps": args.e2e_steps,
@@ -359,14 +369,15 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GUPS", "n_gpus": world,
+            "metric": METRICS[args.config], "value": value, "unit": "GUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic U[0,1) f32 (seeded)",
             "config": {"workload": WORKLOAD_NAME[args.config],
                        "parallelism": f"views sharded x{world}" + (" + NCCL reduce-scatter" if world > 1 else ""),
                        "l2": "inputs (0.5 GiB volume, 1.58 GiB sinogram) exceed L2; no flush",
-                       "voxels": list(spec.shape), "views": g.numViews, "detector": [nr, nc]},
+                       "voxels": list(spec.shape), "views": g.numViews, "detector": [nr, nc],
+                       "batch": B},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": kern[dom]["frac"],
                          "traffic": traffic,

@@ -300,9 +300,16 @@ int ctp_plan_shape(const ctp_plan* plan, int64_t* vol_elems, int64_t* sino_elems
   return CTP_OK;
 }
 
+// fan beam (one slice, one detector row) with a batch: batch-on-lanes kernels
+static bool use_fan_path(const ctp_plan* plan, int batch, uint32_t flags) {
+  return plan->gp.nz == 1 && plan->gp.nr == 1 && batch >= 2 && !(flags & CTP_FLAG_ACCUMULATE);
+}
+
 size_t ctp_sf_workspace_bytes(const ctp_plan* plan, int direction, int batch) {
   if (!plan || batch < 1) return 0;
-  const size_t per = direction == 0 ? plan->vol_elems : plan->sino_elems;
+  size_t per = direction == 0 ? plan->vol_elems : plan->sino_elems;
+  if (plan->gp.nz == 1 && plan->gp.nr == 1 && batch >= 2)
+    per = plan->vol_elems + plan->sino_elems;  // both batch-innermost copies
   return align_up(per * sizeof(float) * (size_t)batch);
 }
 
@@ -315,6 +322,19 @@ int ctp_sf_forward(const ctp_plan* plan, const float* vol, float* sino, int batc
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const GridParams& gp = plan->gp;
+  if (use_fan_path(plan, batch, flags)) {
+    float* xB = static_cast<float*>(workspace);
+    float* yB = xB + plan->vol_elems * (size_t)batch;
+    cudaError_t e = ctp::launch_transpose(vol, xB, batch, (int)plan->vol_elems, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose volume (fan)");
+    KernelTimer timer(plan, 0, s, flags);
+    e = ctp::launch_forward_fan(gp, plan->d_coef, xB, yB, batch, s);
+    timer.stop();
+    if (e != cudaSuccess) return cuda_fail(e, "sf_forward_fan_kernel");
+    e = ctp::launch_transpose(yB, sino, (int)plan->sino_elems, batch, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram (fan)");
+    return CTP_OK;
+  }
   float* xT = static_cast<float*>(workspace);
   cudaError_t e = ctp::launch_transpose(vol, xT, gp.nz, gp.nx * gp.ny, batch, s);
   if (e != cudaSuccess) return cuda_fail(e, "transpose volume");
@@ -334,6 +354,19 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const GridParams& gp = plan->gp;
+  if (use_fan_path(plan, batch, flags)) {
+    float* yB = static_cast<float*>(workspace);
+    float* xB = yB + plan->sino_elems * (size_t)batch;
+    cudaError_t e = ctp::launch_transpose(sino, yB, batch, (int)plan->sino_elems, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram (fan)");
+    KernelTimer timer(plan, 1, s, flags);
+    e = ctp::launch_back_fan(gp, plan->d_coef, yB, xB, batch, s);
+    timer.stop();
+    if (e != cudaSuccess) return cuda_fail(e, "sf_back_fan_kernel");
+    e = ctp::launch_transpose(xB, vol, (int)plan->vol_elems, batch, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose volume (fan)");
+    return CTP_OK;
+  }
   float* yT = static_cast<float*>(workspace);
   cudaError_t e = ctp::launch_transpose(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
   if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram");

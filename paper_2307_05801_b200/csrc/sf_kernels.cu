@@ -834,6 +834,241 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// fan beam (one slice, one detector row) with the batch on the lanes
+// ---------------------------------------------------------------------------
+// BASELINE configs[1]: 64 slices share one geometry, so one footprint setup
+// serves the whole batch.  Layouts are batch-innermost ([pixel][B] volumes,
+// [v][c][B] sinograms, produced by transpose_kernel) so the lanes of a warp
+// (consecutive batch elements) read and write consecutive addresses.  The
+// coefficient association is the same as in the 3D pair:
+//   forward  y += ts * (tt * (amp * x)),   back  x += (amp * tt) * (sum ts * y).
+constexpr int F2_MAXG = 4;  // batch groups of 32 per warp (batch <= 128 per launch)
+
+// axial weight of detector row 0 for slice iz = 0 (boundary rule of the 3D pair)
+__device__ __forceinline__ float row0_weight(float A, float B, float E, bool& hit) {
+  const float T = fma_(B, 0.0f, A);
+  const float lo = add_(T, -E), hi = add_(T, E);
+  const float fl = floorf(add_(lo, -0.5f));
+  const int K = rows_per_slice(B);
+  const int k = -((int)fl + 1);  // row 0 = r0 + k
+  hit = k >= 0 && k < K;
+  if (!hit) return 0.0f;
+  const float lower = (k == 0) ? lo : clampf_(add_(fl, (float)k + 0.5f), lo, hi);
+  const float upper = (k == K - 1) ? hi : clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+  return add_(upper, -lower);
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const ViewCoef* __restrict__ vcoef,
+                                                          const float* __restrict__ yB,  // [nv][nc][Bs]
+                                                          float* __restrict__ xB,        // [ny*nx][Bs]
+                                                          int Bs, int b0, int nb) {
+  __shared__ __align__(16) BkEntry ents[8][32][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pix = blockIdx.x * 8 + warp;
+  if (pix >= gp.nx * gp.ny) return;
+  const int ix = pix % gp.nx, iy = pix / gp.nx;
+  BkEntry(&my)[32][2] = ents[warp];
+  float acc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = 0.0f;
+  for (int vb = 0; vb < gp.nv; vb += 32) {
+    {
+      const int v = vb + lane;
+      BkEntry e0, e1;
+      e0.ncol = 0;
+      e1.ncol = 0;
+      if (v < gp.nv) {
+        const ViewCoef vc = vcoef[v];
+        SubFoot f0, f1;
+        const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
+        if (mask & 1) fill_entry(e0, f0);
+        if (mask & 2) fill_entry(e1, f1);
+      }
+      my[lane][0] = e0;
+      my[lane][1] = e1;
+    }
+    __syncwarp();
+    const int nvb = min(32, gp.nv - vb);
+    for (int j = 0; j < nvb; ++j) {
+#pragma unroll 1
+      for (int s = 0; s < 2; ++s) {
+        const BkEntry e = my[j][s];
+        if (e.ncol == 0) continue;
+        bool hit;
+        const float tt = row0_weight(e.A, e.B, e.E, hit);
+        if (!hit) continue;
+        const float amp = mul_(e.lxy, sqrt_approx(fma_(e.a0, e.a0, 1.0f)));
+        const float c = mul_(amp, tt);
+        const float* yv = yB + (size_t)(vb + j) * gp.nc * Bs + b0;
+        Trap wide{};
+        if (e.ncol > BK_NCF) {
+          SubFoot f0, f1;
+          column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
+          wide = make_trap(s == 0 ? f0 : f1);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int b = lane + 32 * g;
+          if (b >= nb) break;
+          float q = 0.0f;
+          if (e.ncol <= BK_NCF) {
+#pragma unroll
+            for (int k = 0; k < BK_NCF; ++k)
+              if (k < e.ncol) q = fma_(e.ts[k], __ldg(yv + (size_t)(e.cl + k) * Bs + b), q);
+          } else {
+            float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
+            for (int k = 0; k < e.ncol; ++k) {
+              const float cur = trap_cum(wide, add_((float)(e.cl + k), 0.5f));
+              q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + k) * Bs + b), q);
+              prev = cur;
+            }
+          }
+          acc[g] = fma_(c, q, acc[g]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int b = lane + 32 * g;
+    if (b < nb) xB[(size_t)pix * Bs + b0 + b] = acc[g];
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
+    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xB,  // [ny*nx][Bs]
+    float* __restrict__ yB,                                                         // [nv][nc][Bs]
+    int Bs, int b0, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  FwEntry* ent = reinterpret_cast<FwEntry*>(smem_raw) + warp * FV_EBUF;
+  const int ntiles = (gp.nc + FW_CW - 1) / FW_CW;
+  const long long task = (long long)blockIdx.x * FV_WARPS + warp;
+  if (task >= (long long)ntiles * gp.nv) return;
+  const int tile = (int)(task % ntiles);
+  const int v = (int)(task / ntiles);
+  const int c0 = tile * FW_CW;
+  const int cw = min(FW_CW, gp.nc - c0);
+  const ViewCoef vc = vcoef[v];
+  float plx, ply, dlx, dly, phx, phy, dhx, dhy;
+  edge_ray(vc, gp, (float)c0 - 0.5f, plx, ply, dlx, dly);
+  edge_ray(vc, gp, (float)(c0 + cw) - 0.5f, phx, phy, dhx, dhy);
+  const float nl = rsqrtf(dlx * dlx + dly * dly), nh = rsqrtf(dhx * dhx + dhy * dhy);
+  const bool primary_x = fabsf(dlx) * nl + fabsf(dhx) * nh >= fabsf(dly) * nl + fabsf(dhy) * nh;
+  const int nP = primary_x ? gp.nx : gp.ny, nQ = primary_x ? gp.ny : gp.nx;
+  const float halfP = primary_x ? gp.half_x : gp.half_y, halfQ = primary_x ? gp.half_y : gp.half_x;
+  const float lp = primary_x ? plx : ply, lq = primary_x ? ply : plx;
+  const float ldp = primary_x ? dlx : dly, ldq = primary_x ? dly : dlx;
+  const float hp = primary_x ? phx : phy, hq = primary_x ? phy : phx;
+  const float hdp = primary_x ? dhx : dhy, hdq = primary_x ? dhy : dhx;
+  const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
+  const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
+
+  float acc[G][FW_CW];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c = 0; c < FW_CW; ++c) acc[g][c] = 0.0f;
+
+  int pending = 0;
+  auto flush = [&]() {
+    for (int e = 0; e < pending; ++e) {
+      const FwEntry& E = ent[e];
+      bool hit;
+      const float tt = row0_weight(E.A, E.B, E.E, hit);
+      if (!hit) continue;
+      const float amp = mul_(E.lxy, sqrt_approx(fma_(E.a0, E.a0, 1.0f)));
+      const float* xc = xB + (size_t)E.col * Bs + b0;
+      float ts[FW_CW];
+#pragma unroll
+      for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int b = lane + 32 * g;
+        const float xv = b < nb ? __ldg(xc + b) : 0.0f;
+        const float P = mul_(tt, mul_(amp, xv));
+        const float2 pp = bc2_(P);
+#pragma unroll
+        for (int cc = 0; cc < FW_CW; cc += 2) {
+          const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), pp, make_float2(acc[g][cc], acc[g][cc + 1]));
+          acc[g][cc] = a.x;
+          acc[g][cc + 1] = a.y;
+        }
+      }
+    }
+    pending = 0;
+  };
+  const float band_lo = -0.5f, band_hi = (float)gp.nr - 0.5f;
+  for (int ib = 0; ib < nP; ib += 32) {
+    const int i = ib + lane;
+    int jl = 0, cnt = 0;
+    if (i < nP) {
+      int jh = nQ - 1;
+      if (cull) {
+        const float pa = (float)i - halfP, pb = pa + 1.0f;
+        const float q0 = lq + (pa - lp) * lslope, q1 = lq + (pb - lp) * lslope;
+        const float q2 = hq + (pa - hp) * hslope, q3 = hq + (pb - hp) * hslope;
+        const float qmin = fminf(fminf(q0, q1), fminf(q2, q3)) + halfQ;
+        const float qmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) + halfQ;
+        if (qmin > -1e8f && qmax < 1e8f) {
+          jl = max(jl, (int)floorf(qmin) - 1);
+          jh = min(jh, (int)floorf(qmax) + 1);
+        }
+      }
+      cnt = jh >= jl ? jh - jl + 1 : 0;
+    }
+    const int incl = warp_incl_scan(cnt, lane);
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int cbase = 0; cbase < total; cbase += 32) {
+      const int k = cbase + lane;
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, excl, o + step);
+        if (ex <= k) o += step;
+      }
+      const int jo = __shfl_sync(0xffffffffu, jl, o);
+      const int exo = __shfl_sync(0xffffffffu, excl, o);
+      SubFoot f0, f1;
+      int mask = 0, col = 0;
+      if (k < total) {
+        const int ii = ib + o, j = jo + (k - exo);
+        const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
+        col = iy * gp.nx + ix;
+        mask = column_footprint(vc, gp, ix, iy, f0, f1);
+        if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
+        if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
+      }
+      const int n = __popc(mask);
+      const int ni = warp_incl_scan(n, lane);
+      const int off = pending + ni - n;
+      if (mask & 1) write_entry(ent[off], f0, col, c0, cw);
+      if (mask & 2) write_entry(ent[off + (mask & 1)], f1, col, c0, cw);
+      pending += __shfl_sync(0xffffffffu, ni, 31);
+      __syncwarp();
+      if (pending >= 32) {
+        flush();
+        __syncwarp();
+      }
+    }
+  }
+  if (pending > 0) flush();
+  float* yv = yB + (size_t)v * gp.nc * Bs + b0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int b = lane + 32 * g;
+    if (b >= nb) continue;
+#pragma unroll
+    for (int c = 0; c < FW_CW; ++c)
+      if (c < cw) yv[(size_t)(c0 + c) * Bs + b] = acc[g][c];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batch,
@@ -877,6 +1112,45 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
     const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
     sf_forward_kernel<<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xT, sino, accumulate ? 1 : 0, t0,
                                                          ntasks);
+  }
+  return cudaGetLastError();
+}
+
+// xB: [ny*nx][batch]; yB: [nv][nc][batch] (batch-innermost), nz == nr == 1
+cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,
+                               int batch, cudaStream_t st) {
+  const size_t smem = sizeof(FwEntry) * FV_EBUF * FV_WARPS;
+  const long long ntasks = (long long)((gp.nc + FW_CW - 1) / FW_CW) * gp.nv;
+  const unsigned grid = (unsigned)((ntasks + FV_WARPS - 1) / FV_WARPS);
+  for (int b0 = 0; b0 < batch; b0 += 32 * F2_MAXG) {
+    const int nb = min(32 * F2_MAXG, batch - b0);
+    const int G = (nb + 31) / 32;
+    cudaError_t e = cudaSuccess;
+#define CTP_FAN_FWD(g)                                                                              \
+  case g:                                                                                           \
+    e = cudaFuncSetAttribute(sf_forward_fan_kernel<g>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smem);                                                            \
+    if (e != cudaSuccess) return e;                                                                 \
+    sf_forward_fan_kernel<g><<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xB, yB, batch, b0, nb); \
+    break;
+    switch (G) { CTP_FAN_FWD(1) CTP_FAN_FWD(2) CTP_FAN_FWD(3) default: CTP_FAN_FWD(4) }
+#undef CTP_FAN_FWD
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
+                            int batch, cudaStream_t st) {
+  const unsigned grid = (unsigned)((gp.nx * gp.ny + 7) / 8);
+  for (int b0 = 0; b0 < batch; b0 += 32 * F2_MAXG) {
+    const int nb = min(32 * F2_MAXG, batch - b0);
+    const int G = (nb + 31) / 32;
+    switch (G) {
+      case 1: sf_back_fan_kernel<1><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
+      case 2: sf_back_fan_kernel<2><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
+      case 3: sf_back_fan_kernel<3><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
+      default: sf_back_fan_kernel<4><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
+    }
   }
   return cudaGetLastError();
 }

@@ -19,5 +19,10 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
                         int batch, bool accumulate, cudaStream_t st);
 size_t forward_warp_smem_bytes();
+// fan beam (nz == nr == 1) with the batch innermost: xB [ny*nx][batch], yB [nv][nc][batch]
+cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,
+                               int batch, cudaStream_t st);
+cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
+                            int batch, cudaStream_t st);
 
 }  // namespace ctp
