@@ -85,6 +85,13 @@ int validate(const ctp_geom* g) {
     return fail(CTP_ERR_INVALID_ARGUMENT, "array too large");
   for (long long k = 0; k < 15LL * g->num_views; ++k)
     if (!std::isfinite(g->poses[k])) return fail(CTP_ERR_INVALID_ARGUMENT, "non-finite pose entry");
+  if (g->kind == CTP_MODULAR) {
+    // the SF-modular model keeps detector rows increasing with z
+    for (int v = 0; v < g->num_views; ++v)
+      if (!(g->poses[15 * v + 11] > 0.05))
+        return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
+                    "SF-modular needs rowDir with a positive z component (> 0.05) in every view");
+  }
   return CTP_OK;
 }
 
@@ -124,6 +131,39 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
       c.tc = (float)(hx * vax[1] / ph);
       c.tz = (float)(hz * vax[2] / ph);
       c.cull = 1;
+      continue;
+    }
+    if (g.kind == CTP_MODULAR) {
+      // flat panel in an arbitrary pose (extension): the
+      // transverse trapezoid is taken at the grid's centre height zr with the
+      // full 3-D ray/plane intersection, the axial map from the column centre
+      // line (affine in z for a detector whose normal is horizontal)
+      const double nxv = u[1] * vax[2] - u[2] * vax[1];
+      const double nyv = u[2] * vax[0] - u[0] * vax[2];
+      const double nzv = u[0] * vax[1] - u[1] * vax[0];
+      const double lamnum = (c0[0] - s[0]) * nxv + (c0[1] - s[1]) * nyv + (c0[2] - s[2]) * nzv;
+      const double zr = g.z0 + 0.5 * g.num_z * hz;
+      c.dxa = (float)(xm - s[0]);
+      c.dya = (float)(ym - s[1]);
+      c.zc0 = (float)(g.z0 + 0.5 * hz - s[2]);
+      c.na = (float)((xm - s[0]) * u[0] + (ym - s[1]) * u[1] + (zr - s[2]) * u[2]);
+      c.nb = (float)(hx * u[0]);
+      c.nc = (float)(hx * u[1]);
+      c.da = (float)((xm - s[0]) * nxv + (ym - s[1]) * nyv + (zr - s[2]) * nzv);
+      c.db = (float)(hx * nxv);
+      c.dc = (float)(hx * nyv);
+      c.dm = c.da;
+      c.s0 = (float)(((s[0] - c0[0]) * u[0] + (s[1] - c0[1]) * u[1] + (s[2] - c0[2]) * u[2]) / pw + cc);
+      c.g = (float)(lamnum / pw);
+      c.lamnum = (float)lamnum;
+      c.ta = (float)(((s[0] - c0[0]) * vax[0] + (s[1] - c0[1]) * vax[1] + (s[2] - c0[2]) * vax[2]) / ph + cr);
+      c.tb = (float)(hx * vax[0] / ph);
+      c.tc = (float)(hx * vax[1] / ph);
+      c.tz = (float)vax[2];
+      c.tva = (float)(((xm - s[0]) * vax[0] + (ym - s[1]) * vax[1]) / ph);
+      const bool inside = std::fabs((s[0] - xm) / hx) < half_x + 2.0 &&
+                          std::fabs((s[1] - ym) / hx) < half_y + 2.0;
+      c.cull = inside ? 0 : 1;
       continue;
     }
     // cone: plane normal and lamnum (_kernels.py:562-569)
@@ -196,9 +236,6 @@ int check_run_args(const ctp_plan* plan, const void* in, const void* out, int ba
   if (!in || !out) return fail(CTP_ERR_INVALID_ARGUMENT, "null data pointer");
   if (batch < 1) return fail(CTP_ERR_INVALID_ARGUMENT, "batch must be >= 1");
   if (in == out) return fail(CTP_ERR_INVALID_ARGUMENT, "input and output must not alias");
-  if (plan->geom.kind == CTP_MODULAR)
-    return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
-                "separable-footprint projector does not support modular geometry");
   if (ws_bytes < need || (need > 0 && !ws))
     return fail(CTP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
   return CTP_OK;

@@ -56,7 +56,8 @@ struct alignas(16) ViewCoef {
   float xc0, yc0;        // detector reference point c0 in centred grid-index coords
   int cull;              // 1: wedge culling is safe for this view (source outside grid)
   int split_x;           // _sf_subdivide axis decided in f64: |u_x| hx >= |u_y| hx
-  float pad[3];
+  float tva;             // modular: ((xm-sx) v_x + (ym-sy) v_y) / ph
+  float pad[2];
 };
 static_assert(sizeof(ViewCoef) == 128, "ViewCoef must stay 128 bytes");
 
@@ -262,11 +263,22 @@ __device__ __forceinline__ bool sub_footprint(const ViewCoef& v, const GridParam
     }
     dxn = div_(dx, rho);
     dyn = div_(dy, rho);
-    // axial: tcen = mag*(cz - src_z)  (_kernels.py:626-628), in row units
-    const float bm = mul_(mag, gp.hz_over_ph);
-    f.B = bm;
-    f.E = mul_(0.5f, bm);
-    f.A = fma_(mul_(mag, v.zc0), gp.inv_ph, gp.cr);
+    if (gp.kind == kModular) {
+      // modular (extension): row coordinate of the column centre
+      // line t(z) = (src-c0).v + mag ((c-src)_xy . v_xy + v_z (z - src_z)),
+      // affine in z; ta = (src-c0).v/ph + cr, tb/tc/tva the xy part, tz = v_z
+      const float txy = affine_(v.tva, v.tb, v.tc, X, Y);
+      const float bm = mul_(mag, mul_(v.tz, gp.hz_over_ph));
+      f.B = bm;
+      f.E = mul_(0.5f, bm);
+      f.A = fma_(mag, fma_(mul_(v.tz, gp.inv_ph), v.zc0, txy), v.ta);
+    } else {
+      // axial: tcen = mag*(cz - src_z)  (_kernels.py:626-628), in row units
+      const float bm = mul_(mag, gp.hz_over_ph);
+      f.B = bm;
+      f.E = mul_(0.5f, bm);
+      f.A = fma_(mul_(mag, v.zc0), gp.inv_ph, gp.cr);
+    }
     f.a0 = div_(v.zc0, rho);
     f.a1 = div_(gp.hz, rho);
   }

@@ -466,6 +466,18 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
     dy = cs * vc.wy + sn * vc.uy;
     return;
   }
+  if (gp.kind == kModular) {
+    // line {S(X, Y) = S} at the reference height: g num - (S - s0) den = 0
+    const float kk = S - vc.s0;
+    const float al = vc.g * vc.nb - kk * vc.db, be = vc.g * vc.nc - kk * vc.dc;
+    const float ga = vc.g * vc.na - kk * vc.da;
+    const float n2 = al * al + be * be;
+    px = -ga * al / n2;
+    py = -ga * be / n2;
+    dx = be;
+    dy = -al;
+    return;
+  }
   const float k = s_mm / gp.hx;
   px = vc.xc0 + k * vc.ux;
   py = vc.yc0 + k * vc.uy;

@@ -265,3 +265,47 @@ def test_fan_batch_against_oracle_and_golden(golden, oracle_mod):
 
 def test_c2_fan_batch40_subset(oracle_mod):
     _parity(oracle_mod, C2, batch=40, views=list(range(0, 720, 45)))
+
+
+# ---------------------------------------------------------------------------
+# SF-modular (extension: the reference has no SF for modular geometry)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["cone_small", "offset_cone", "c3_optics", "split_cone"])
+def test_modular_of_cone_flat_equals_cone_flat(golden, name):
+    c = golden[name]
+    P = pair_of(c["config"])
+    Pm = ct.ProjectorPair(ct.SF, ct.to_modular(P.geometry), P.volumeSpec)
+    x = torch.from_numpy(c["x"]).to(DEV)[None]
+    y = torch.from_numpy(c["y"]).to(DEV)[None]
+    assert rel_l2(ct.forward(Pm, x).cpu(), ct.forward(P, x).cpu()) < 1e-5
+    assert rel_l2(ct.adjoint(Pm, y).cpu(), ct.adjoint(P, y).cpu()) < 1e-5
+    # and therefore matches the reference cone-flat outputs
+    assert rel_l2(ct.forward(Pm, x)[0].cpu().numpy(), c["fwd"]) <= REL_L2_TOL
+
+
+def _perturbed(n=6, views=10, seed=1):
+    from paper_2307_05801_b200 import configs
+
+    cfg = dict(geometry="modular", numX=n, numY=n, numZ=n - 1, voxelWidth=1.5, voxelHeight=1.4,
+               numRows=9, numCols=11, pixelHeight=1.7, pixelWidth=1.6,
+               views=configs.modular_orbit(views, 40.0, 90.0, seed=seed, dz=4.0, rot_deg=5.0,
+                                           shift=2.0))
+    return pair_of(cfg)
+
+
+def test_modular_perturbed_exact_transpose():
+    P = _perturbed()
+    n = P.volumeSpec.num_voxels
+    m = int(np.prod(P.geometry.shape))
+    A = dev_fwd(P, torch.eye(n, device=DEV)).reshape(n, m).T.cpu().numpy()
+    B = dev_back(P, torch.eye(m, device=DEV)).reshape(m, n).T.cpu().numpy()
+    assert np.abs(A).sum() > 0
+    assert np.array_equal(A, B.T), np.abs(A - B.T).max()
+
+
+def test_c4_modular_adjoint():
+    from paper_2307_05801_b200 import configs
+
+    P = pair_of(configs.c4(360, seed=0))
+    rep = ct.adjoint_check(P, trials=2, seed=0)
+    assert rep["maxRelErr"] < ADJOINT_TOL, rep

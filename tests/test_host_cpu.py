@@ -104,8 +104,15 @@ def test_pair_model_checks():
     g, spec = ct.parse_config(json.dumps(BASE))
     with pytest.raises(errors.SpecMismatchError):
         ct.ProjectorPair("fancy", g, spec)
+    # SF-modular is an extension of this build; poses whose rows do not point
+    # upward are rejected
+    ct.ProjectorPair(ct.SF, ct.to_modular(g), spec)
+    gm = ct.to_modular(g)
+    flipped = tuple(ct.ModularView(mv.sourcePos, mv.detectorCenter, -mv.rowDir, mv.colDir)
+                    for mv in gm.modularViews)
     with pytest.raises(errors.UnsupportedGeometryError):
-        ct.ProjectorPair(ct.SF, ct.to_modular(g), spec)
+        ct.ProjectorPair(ct.SF, ct.Geometry(kind=ct.MODULAR, detector=g.detector,
+                                            modularViews=flipped), spec)
     with pytest.raises(errors.UnsupportedGeometryError):
         ct.ProjectorPair(ct.SIDDON, g, spec)
 
@@ -173,6 +180,17 @@ def test_no_silent_cpu_fallback():
 def _declared_functions():
     text = open(HEADER).read()
     return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(ctp_\w+)\s*\(", text, re.M)))
+
+
+def test_c4_pose_generator_is_seeded_and_valid():
+    from paper_2307_05801_b200 import configs
+
+    a, b = configs.c4(12, seed=3), configs.c4(12, seed=3)
+    assert a == b
+    g, spec = ct.parse_config(json.dumps(a))
+    assert g.kind == ct.MODULAR and g.shape == (12, 384, 384) and spec.shape == (256, 256, 256)
+    for mv in g.modularViews:
+        assert mv.rowDir[2] > 0.99
 
 
 def test_header_declarations_match_binding_list():
