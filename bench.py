@@ -43,6 +43,9 @@ CONFIGS = {
     "c2": dict(geometry="cone", numX=512, numY=512, numZ=1, voxelWidth=0.6667,
                voxelHeight=1.0, numRows=1, numCols=768, pixelHeight=1.0, pixelWidth=1.0,
                sod=1000.0, sdd=1500.0, numAngles=720, angularRange=360.0),
+    "c5": dict(geometry="cone", numX=1024, numY=1024, numZ=1024, voxelWidth=0.3333,
+               voxelHeight=0.3333, numRows=1536, numCols=1536, pixelHeight=0.5, pixelWidth=0.5,
+               sod=1000.0, sdd=1500.0, numAngles=1440, angularRange=360.0),
     "c1": dict(geometry="parallel", numX=128, numY=128, numZ=128, voxelWidth=1.0,
                voxelHeight=1.0, numRows=128, numCols=128, pixelHeight=1.0, pixelWidth=1.0,
                numAngles=180, angularRange=180.0),
@@ -51,10 +54,12 @@ WORKLOAD_NAME = {
     "c3": "cone-beam flat 512^3 x 720 views, 768^2 det, fwd+back (BASELINE configs[2])",
     "c1": "parallel-beam 128^3 x 180 views, 128^2 det, fwd+back (BASELINE configs[0])",
     "c2": "fan-beam (cone-flat, 1 row, 1 slice) 512^2 x batch 64 x 720 views, 768 cols (BASELINE configs[1])",
+    "c5": "cone-beam flat 1024^3 x 1440 views, 1536^2 det, fwd+back (BASELINE configs[4])",
 }
 METRIC = "fwd+back projector GUPS, cone-beam 512³ × 720 views"
 METRICS = {"c3": METRIC, "c1": "fwd+back projector GUPS, parallel-beam 128³ × 180 views",
-           "c2": "fwd+back projector GUPS, fan-beam 512² × batch 64 × 720 views"}
+           "c2": "fwd+back projector GUPS, fan-beam 512² × batch 64 × 720 views",
+           "c5": "fwd+back projector GUPS, cone-beam 1024³ × 1440 views"}
 
 
 def _peaks():

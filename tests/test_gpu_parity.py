@@ -309,3 +309,9 @@ def test_c4_modular_adjoint():
     P = pair_of(configs.c4(360, seed=0))
     rep = ct.adjoint_check(P, trials=2, seed=0)
     assert rep["maxRelErr"] < ADJOINT_TOL, rep
+
+
+def test_c5_cone_view_subset(oracle_mod):
+    from paper_2307_05801_b200 import configs
+
+    _parity(oracle_mod, configs.C5, views=[5, 700])
