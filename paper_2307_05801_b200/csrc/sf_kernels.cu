@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
     float* __restrict__ out, int accumulate) {
   __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
-  __shared__ float qbuf[BK_WARPS][BK_QMAX];
+  __shared__ __align__(16) float qbuf[BK_WARPS][BK_QMAX + 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbx = (gp.nx + 3) >> 2;
   const int ix = (blockIdx.x % nbx) * 4 + (warp & 3);
@@ -284,6 +284,36 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           const float t1 = e.ncol > 1 ? e.ts[1] : 0.0f;
           const float t2 = e.ncol > 2 ? e.ts[2] : 0.0f;
           const float t3 = e.ncol > 3 ? e.ts[3] : 0.0f;
+          if (Ra >= 0 && Rz < nr && (nr & 3) == 0) {
+            // 4 consecutive rows per lane and iteration (16-byte loads); the
+            // table starts at Ra4 = Ra & ~3 and ends at (Rz | 3) < nr
+            const int Ra4 = Ra & ~3;
+            const int n4 = ((Rz | 3) - Ra4 + 1) >> 2;
+            const float4* v0 = reinterpret_cast<const float4*>(p0 + Ra4);
+            const float4* v1 = reinterpret_cast<const float4*>(p1 + Ra4);
+            const float4* v2 = reinterpret_cast<const float4*>(p2 + Ra4);
+            const float4* v3 = reinterpret_cast<const float4*>(p3 + Ra4);
+            const float2 T0 = bc2_(t0), T1 = bc2_(t1), T2 = bc2_(t2), T3 = bc2_(t3);
+            float4* q4 = reinterpret_cast<float4*>(qw);
+            for (int t = lane; t < n4; t += 32) {
+              const float4 a = __ldg(v0 + t), bq = __ldg(v1 + t), cq = __ldg(v2 + t), d = __ldg(v3 + t);
+              float2 lo = mul2_(T0, make_float2(a.x, a.y));
+              float2 hi = mul2_(T0, make_float2(a.z, a.w));
+              lo = fma2_(T1, make_float2(bq.x, bq.y), lo);
+              hi = fma2_(T1, make_float2(bq.z, bq.w), hi);
+              lo = fma2_(T2, make_float2(cq.x, cq.y), lo);
+              hi = fma2_(T2, make_float2(cq.z, cq.w), hi);
+              lo = fma2_(T3, make_float2(d.x, d.y), lo);
+              hi = fma2_(T3, make_float2(d.z, d.w), hi);
+              q4[t] = make_float4(lo.x, lo.y, hi.x, hi.y);
+            }
+            __syncwarp();
+            if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Ra4);
+            else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, Ra4);
+            else back_slices<4>(acc, e, izf0, nvalid, qw, Ra4);
+            __syncwarp();
+            continue;
+          }
           if (Ra >= 0 && Rz < nr) {
             // rows r and r + 32 per iteration, packed
             const float2 T0 = bc2_(t0), T1 = bc2_(t1), T2 = bc2_(t2), T3 = bc2_(t3);
