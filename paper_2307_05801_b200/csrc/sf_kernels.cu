@@ -92,7 +92,7 @@ __device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&
 constexpr int BK_WARPS = 8;
 constexpr int BK_ZPL = 8;           // voxels per lane
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
-constexpr int BK_QMAX = 560;        // per-warp row-sum table (rows): ZC * 2 + margin
+constexpr int BK_QMAX = 480;        // per-warp row-sum table (rows): ZC * 1.8 + margin
 constexpr int BK_NCF = 4;           // footprint columns handled by the table path
 
 struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
@@ -100,11 +100,16 @@ struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
   float a0, a1;
   int cl;
   int ncol;  // 0: no contribution; > BK_NCF: wide footprint (direct path)
-  float ts[BK_NCF];
+  float ts[BK_NCF];  // 0 beyond ncol
+  // precomputed by the lane-parallel setup for the fast path:
+  int off0;  // (cl * nr + ra4): element offset of the first table row, column cl
+  int pk;    // bit 0: fast path; bits 1-3: K; bits 4-15: n4; bits 16-31: ra4
+  int pad[2];
 };
-static_assert(sizeof(BkEntry) == 48, "BkEntry layout");
+static_assert(sizeof(BkEntry) == 64, "BkEntry layout");
 
-__device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f) {
+__device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const GridParams& gp,
+                                           int izs, int ize) {
   e.A = f.A; e.B = f.B; e.E = f.E; e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
   e.cl = f.cl;
   e.ncol = f.ch >= f.cl ? f.ch - f.cl + 1 : 0;
@@ -112,7 +117,17 @@ __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f) {
   float ts[BK_NCF];
   col_weights<BK_NCF>(p, f.cl, ts);
 #pragma unroll
-  for (int k = 0; k < BK_NCF; ++k) e.ts[k] = ts[k];
+  for (int k = 0; k < BK_NCF; ++k) e.ts[k] = k < e.ncol ? ts[k] : 0.0f;
+  const int K = rows_per_slice(f.B);
+  const int Ra = first_row(sub_(fma_(f.B, (float)izs, f.A), f.E));
+  const int Rz = first_row(sub_(fma_(f.B, (float)ize, f.A), f.E)) + K - 1;
+  const int ra4 = Ra & ~3;
+  const int n4 = ((Rz | 3) - ra4 + 1) >> 2;
+  const bool fast = e.ncol > 0 && e.ncol <= BK_NCF && f.cl + 3 <= gp.nc - 1 && K <= 4 && Ra >= 0 &&
+                    Rz < gp.nr && (gp.nr & 3) == 0 && 4 * n4 <= BK_QMAX + 8 && n4 < 4096;
+  e.pk = fast ? (1 | (K << 1) | (n4 << 4) | (ra4 << 16)) : 0;
+  e.off0 = fast ? f.cl * gp.nr + ra4 : 0;
+  if (Rz < 0 || Ra > gp.nr - 1) e.ncol = 0;  // entirely off the detector
 }
 
 // Direct (table-free) contribution of one voxel: rows r0..r0+K-1, any
@@ -254,8 +269,8 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
         const ViewCoef vc = vcoef[v];
         SubFoot f0, f1;
         const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if (mask & 1) fill_entry(e0, f0);
-        if (mask & 2) fill_entry(e1, f1);
+        if (mask & 1) fill_entry(e0, f0, gp, izs, ize);
+        if (mask & 2) fill_entry(e1, f1, gp, izs, ize);
       }
       my[lane][0] = e0;
       my[lane][1] = e1;
@@ -265,7 +280,40 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     for (int j = 0; j < nvb; ++j) {
 #pragma unroll 1
       for (int s = 0; s < 2; ++s) {
-        const BkEntry e = my[j][s];
+        const BkEntry& ef = my[j][s];
+        const int pk = ef.pk;
+        if (pk & 1) {
+          // fast path: everything precomputed; 4-row float4 row sums, then slices
+          const float* yv = yb + (size_t)(vb + j) * view_elems + ef.off0;
+          const float4* v0 = reinterpret_cast<const float4*>(yv);
+          const float4* v1 = reinterpret_cast<const float4*>(yv + nr);
+          const float4* v2 = reinterpret_cast<const float4*>(yv + 2 * nr);
+          const float4* v3 = reinterpret_cast<const float4*>(yv + 3 * nr);
+          const float2 T0 = bc2_(ef.ts[0]), T1 = bc2_(ef.ts[1]), T2 = bc2_(ef.ts[2]), T3 = bc2_(ef.ts[3]);
+          const int n4 = (pk >> 4) & 0xfff;
+          float4* q4 = reinterpret_cast<float4*>(qw);
+          for (int t = lane; t < n4; t += 32) {
+            const float4 a = __ldg(v0 + t), bq = __ldg(v1 + t), cq = __ldg(v2 + t), d = __ldg(v3 + t);
+            float2 lo = mul2_(T0, make_float2(a.x, a.y));
+            float2 hi = mul2_(T0, make_float2(a.z, a.w));
+            lo = fma2_(T1, make_float2(bq.x, bq.y), lo);
+            hi = fma2_(T1, make_float2(bq.z, bq.w), hi);
+            lo = fma2_(T2, make_float2(cq.x, cq.y), lo);
+            hi = fma2_(T2, make_float2(cq.z, cq.w), hi);
+            lo = fma2_(T3, make_float2(d.x, d.y), lo);
+            hi = fma2_(T3, make_float2(d.z, d.w), hi);
+            q4[t] = make_float4(lo.x, lo.y, hi.x, hi.y);
+          }
+          __syncwarp();
+          const int K = (pk >> 1) & 7, ra4 = pk >> 16;
+          const BkEntry e = ef;
+          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, ra4);
+          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, ra4);
+          else back_slices<4>(acc, e, izf0, nvalid, qw, ra4);
+          __syncwarp();
+          continue;
+        }
+        const BkEntry e = ef;
         if (e.ncol == 0) continue;
         const int K = rows_per_slice(e.B);
         const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
@@ -284,36 +332,6 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           const float t1 = e.ncol > 1 ? e.ts[1] : 0.0f;
           const float t2 = e.ncol > 2 ? e.ts[2] : 0.0f;
           const float t3 = e.ncol > 3 ? e.ts[3] : 0.0f;
-          if (Ra >= 0 && Rz < nr && (nr & 3) == 0) {
-            // 4 consecutive rows per lane and iteration (16-byte loads); the
-            // table starts at Ra4 = Ra & ~3 and ends at (Rz | 3) < nr
-            const int Ra4 = Ra & ~3;
-            const int n4 = ((Rz | 3) - Ra4 + 1) >> 2;
-            const float4* v0 = reinterpret_cast<const float4*>(p0 + Ra4);
-            const float4* v1 = reinterpret_cast<const float4*>(p1 + Ra4);
-            const float4* v2 = reinterpret_cast<const float4*>(p2 + Ra4);
-            const float4* v3 = reinterpret_cast<const float4*>(p3 + Ra4);
-            const float2 T0 = bc2_(t0), T1 = bc2_(t1), T2 = bc2_(t2), T3 = bc2_(t3);
-            float4* q4 = reinterpret_cast<float4*>(qw);
-            for (int t = lane; t < n4; t += 32) {
-              const float4 a = __ldg(v0 + t), bq = __ldg(v1 + t), cq = __ldg(v2 + t), d = __ldg(v3 + t);
-              float2 lo = mul2_(T0, make_float2(a.x, a.y));
-              float2 hi = mul2_(T0, make_float2(a.z, a.w));
-              lo = fma2_(T1, make_float2(bq.x, bq.y), lo);
-              hi = fma2_(T1, make_float2(bq.z, bq.w), hi);
-              lo = fma2_(T2, make_float2(cq.x, cq.y), lo);
-              hi = fma2_(T2, make_float2(cq.z, cq.w), hi);
-              lo = fma2_(T3, make_float2(d.x, d.y), lo);
-              hi = fma2_(T3, make_float2(d.z, d.w), hi);
-              q4[t] = make_float4(lo.x, lo.y, hi.x, hi.y);
-            }
-            __syncwarp();
-            if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Ra4);
-            else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, Ra4);
-            else back_slices<4>(acc, e, izf0, nvalid, qw, Ra4);
-            __syncwarp();
-            continue;
-          }
           if (Ra >= 0 && Rz < nr) {
             // rows r and r + 32 per iteration, packed
             const float2 T0 = bc2_(t0), T1 = bc2_(t1), T2 = bc2_(t2), T3 = bc2_(t3);
@@ -924,8 +942,8 @@ __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const V
         const ViewCoef vc = vcoef[v];
         SubFoot f0, f1;
         const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if (mask & 1) fill_entry(e0, f0);
-        if (mask & 2) fill_entry(e1, f1);
+        if (mask & 1) fill_entry(e0, f0, gp, 0, 0);
+        if (mask & 2) fill_entry(e1, f1, gp, 0, 0);
       }
       my[lane][0] = e0;
       my[lane][1] = e1;
