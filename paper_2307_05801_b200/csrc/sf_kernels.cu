@@ -707,16 +707,20 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
     }
     if (e == e_pf) {
       // stage (lo, hi, amp*x) of slices za..zb between zero sentinels
+      // two 32-slice chunks per step in packed f32x2 (same IEEE ops as scalar)
 #pragma unroll
-      for (int t = 0; t < FW_NPF; ++t) {
+      for (int t = 0; t < FW_NPF; t += 2) {
         const int i = lane + 32 * t;
-        if (i < nvox_all) {
-          const float izf = (float)(za + i);
-          const float T = fma_(B, izf, A);
-          const float q = fma_(a1, izf, a0);
-          const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-          sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, xr[t]), 0.0f);
-        }
+        if (32 * t >= nvox_all) break;  // warp-uniform
+        const float2 izf = make_float2((float)(za + i), (float)(za + i + 32));
+        const float2 T = fma2_(bc2_(B), izf, bc2_(A));
+        const float2 q = fma2_(bc2_(a1), izf, bc2_(a0));
+        const float2 tq = fma2_(q, q, bc2_(1.0f));
+        const float2 amp = mul2_(bc2_(lxy), make_float2(sqrt_approx(tq.x), sqrt_approx(tq.y)));
+        const float2 lo = add2_(T, bc2_(-Eh)), hi = add2_(T, bc2_(Eh));
+        const float2 xa = mul2_(amp, make_float2(xr[t], t + 1 < FW_NPF ? xr[t + 1] : 0.0f));
+        if (i < nvox_all) sw[FW_PAD + i] = make_float4(lo.x, hi.x, xa.x, 0.0f);
+        if (i + 32 < nvox_all) sw[FW_PAD + i + 32] = make_float4(lo.y, hi.y, xa.y, 0.0f);
       }
       if (lane < FW_PAD) sw[FW_PAD + nvox_all + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
       __syncwarp();
@@ -781,8 +785,11 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
   if (task >= ntasks) return;  // warp-uniform; no CTA barriers in this kernel
   const int nbands = (gp.nr + FW_ROWS - 1) / FW_ROWS;
   const int ntiles = (gp.nc + FW_CW - 1) / FW_CW;
-  const int band = (int)(task % nbands);
-  const long long t2 = task / nbands;
+  // band-major task order: consecutive CTAs sweep views and tiles of one row
+  // band, i.e. the same z-range of the volume, which then stays in L2
+  const long long per_band = (long long)ntiles * gp.nv * gp.batch;
+  const int band = (int)(task / per_band);
+  const long long t2 = task % per_band;
   const int tile = (int)(t2 % ntiles);
   const int vb = (int)(t2 / ntiles);
   const int v = vb % gp.nv, b = vb / gp.nv;
@@ -1166,11 +1173,13 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
   const long long ntiles = (gp.nc + FW_CW - 1) / FW_CW;
   const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
   const long long max_blocks = 1LL << 30;
+  GridParams g2 = gp;
+  g2.batch = batch;  // the task decode needs the batch extent
   for (long long t0 = 0; t0 < ntasks; t0 += max_blocks * FV_WARPS) {
     const long long rem = ntasks - t0;
     const long long nb = (rem + FV_WARPS - 1) / FV_WARPS;
     const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
-    sf_forward_kernel<<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xT, sino, accumulate ? 1 : 0, t0,
+    sf_forward_kernel<<<grid, FV_WARPS * 32, smem, st>>>(g2, vcoef, xT, sino, accumulate ? 1 : 0, t0,
                                                          ntasks);
   }
   return cudaGetLastError();
