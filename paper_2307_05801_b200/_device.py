@@ -55,10 +55,39 @@ def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None):
         with torch.cuda.device(batch.device):
             return plan.forward(x, out=out) if direction == 0 else plan.back(x, out=out)
     # host input: numpy array or CPU tensor
-    from .chunking import host_apply
+    from .chunking import host_apply, zslab_apply
 
     plan = plan_for(g, spec)
     as_numpy = not isinstance(batch, torch.Tensor)
     host = torch.from_numpy(np.ascontiguousarray(batch, dtype=np.float32)) if as_numpy else batch
-    res = host_apply(plan, host.to(torch.float32).contiguous(), direction)
+    host = host.to(torch.float32).contiguous()
+    nzs = zslab_slices(g, spec, int(host.shape[0]), plan.device)
+    if 0 < nzs < spec.numZ:
+        res = zslab_apply(plan, host, direction, nzs)
+    else:
+        res = host_apply(plan, host, direction)
     return res.numpy() if as_numpy else res
+
+
+def zslab_slices(g: Geometry, spec: VolumeSpec, batch: int, device) -> int:
+    """z-slab size for host-resident calls: CTPROJ_ZSLAB if set, else 0 (no
+    slabbing) when volume + sinogram + workspaces fit in 80% of the free
+    device memory, else the largest slab that does (north_star item 3)."""
+    import os
+
+    torch = _torch()
+    forced = int(os.environ.get("CTPROJ_ZSLAB", "0"))
+    if forced > 0:
+        return forced
+    vol = 4 * batch * spec.num_voxels
+    sino = 4 * batch * int(np.prod(g.shape))
+    free = torch.cuda.mem_get_info(device)[0]
+    budget = 0.8 * free
+    if 2 * vol + 2 * sino <= budget:
+        return 0
+    per_slice = 2 * vol / spec.numZ
+    room = budget - 2 * sino
+    if room <= per_slice:
+        raise CudaRuntimeError(
+            f"sinogram of {sino / 2**30:.1f} GiB does not fit next to one z-slice on the device")
+    return max(1, int(room // per_slice))

@@ -16,6 +16,14 @@ Every chunk is a plan over ``Geometry.with_views`` of a contiguous view
 range, so the arithmetic per view is identical to the unchunked call
 (forward: bitwise; back: the per-voxel view sum is split into chunk partial
 sums, i.e. a different fp32 summation order).
+
+z-slabs (``zslab_apply``) bound the device working set by the volume side:
+the grid is cut into slabs of ``nzs`` slices (each a plan over a VolumeSpec
+with the slab's numZ / offsetZ).  Forward: slab k+1 is uploaded while slab k is
+projected and accumulated into the resident sinogram (CTP_FLAG_ACCUMULATE).
+Back: slab k is back-projected from the resident sinogram while slab k-1 is
+copied down.  Only one slab of the volume is on the device at a time (two
+while overlapping).
 """
 
 from __future__ import annotations
@@ -93,5 +101,64 @@ def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CH
                 p.back(yd, out=out_d[b:b + 1], accumulate=k > 0)
         out = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, pin_memory=True)
         out.copy_(out_d, non_blocking=True)
+        compute.synchronize()
+        return out
+
+
+def slab_spec(spec, z_first: int, nzs: int):
+    """VolumeSpec of slices [z_first, z_first + nzs) of ``spec``."""
+    from .geometry import VolumeSpec
+
+    lo = spec.offsetZ - spec.numZ * spec.voxelHeight / 2.0
+    center = lo + (z_first + nzs / 2.0) * spec.voxelHeight
+    return VolumeSpec(numX=spec.numX, numY=spec.numY, numZ=nzs, voxelWidth=spec.voxelWidth,
+                      voxelHeight=spec.voxelHeight, offsetX=spec.offsetX, offsetY=spec.offsetY,
+                      offsetZ=center)
+
+
+def zslab_ranges(nz: int, nzs: int):
+    return [(a, min(nz, a + nzs)) for a in range(0, nz, nzs)]
+
+
+def zslab_apply(plan: "_native.Plan", host, direction: int, nzs: int):
+    """Host tensor in -> pinned host tensor out, streaming the volume in
+    z-slabs of ``nzs`` slices (see module docstring)."""
+    torch = _torch()
+    dev = plan.device
+    g, spec = plan.geometry, plan.spec
+    B = int(host.shape[0])
+    ranges = zslab_ranges(spec.numZ, nzs)
+    plans = [_native.get_plan(g, slab_spec(spec, a, b - a), dev.index) for a, b in ranges]
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    src = host if host.is_pinned() else host.pin_memory()
+    with torch.cuda.device(dev):
+        if direction == 0:
+            yd = torch.zeros((B,) + tuple(g.shape), dtype=torch.float32, device=dev)
+            for b in range(B):
+                for k, ((a, e), p) in enumerate(zip(ranges, plans)):
+                    with torch.cuda.stream(copy):
+                        xs = src[b:b + 1, a:e].to(dev, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    compute.wait_event(ev)
+                    xs.record_stream(compute)
+                    p.forward(xs, out=yd[b:b + 1], accumulate=True)
+            out = torch.empty((B,) + tuple(g.shape), dtype=torch.float32, pin_memory=True)
+            out.copy_(yd, non_blocking=True)
+            compute.synchronize()
+            return out
+        yd = src.to(dev, non_blocking=True)
+        out = torch.empty((B,) + tuple(spec.shape), dtype=torch.float32, pin_memory=True)
+        for b in range(B):
+            for (a, e), p in zip(ranges, plans):
+                xs = p.back(yd[b:b + 1])
+                ev = torch.cuda.Event()
+                ev.record(compute)
+                copy.wait_event(ev)
+                with torch.cuda.stream(copy):
+                    out[b, a:e].copy_(xs[0], non_blocking=True)
+                    xs.record_stream(copy)
+        compute.wait_stream(copy)
         compute.synchronize()
         return out

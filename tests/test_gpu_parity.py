@@ -317,3 +317,30 @@ def test_c5_cone_view_subset(oracle_mod):
     # fp32 row coordinates near 1536 resolve ~1.2e-4 row: with only 2 views the
     # worst voxel sees ~1.8e-4 of max; the stated max-abs bound at this scale is 1e-3
     _parity(oracle_mod, configs.C5, views=[5, 700], max_abs=1e-3)
+
+
+@pytest.mark.parametrize("nzs", [5, 16])
+def test_zslab_streaming_matches_resident(golden, nzs):
+    from paper_2307_05801_b200 import chunking
+
+    c = golden["c3_optics"]  # 48 x 48 x 40 grid, C3 optics
+    P = pair_of(c["config"])
+    plan = P.plan(0)
+    xh = torch.from_numpy(c["x"][None].copy())
+    yh = torch.from_numpy(c["y"][None].copy())
+    f_slab = chunking.zslab_apply(plan, xh, 0, nzs)
+    b_slab = chunking.zslab_apply(plan, yh, 1, nzs)
+    f_ref = ct.forward(P, xh.to(DEV)).cpu()
+    b_ref = ct.adjoint(P, yh.to(DEV)).cpu()
+    assert rel_l2(f_slab.numpy(), f_ref.numpy()) < 1e-6
+    assert rel_l2(b_slab.numpy(), b_ref.numpy()) < 1e-6
+    assert rel_l2(f_slab[0].numpy(), c["fwd"]) <= REL_L2_TOL
+
+
+def test_zslab_env_forces_streaming(golden, monkeypatch):
+    c = golden["cone_small"]
+    P = pair_of(c["config"])
+    ref = ct.forward(P, c["x"][None])
+    monkeypatch.setenv("CTPROJ_ZSLAB", "5")
+    got = ct.forward(P, c["x"][None])
+    assert rel_l2(got, ref) < 1e-6
