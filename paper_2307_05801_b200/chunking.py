@@ -60,12 +60,13 @@ def chunk_plans(plan: "_native.Plan", ranges):
 
 def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CHUNK_BYTES):
     """Apply A (direction 0) / A^T (1) to a host f32 tensor [B, ...]; returns
-    a pinned host tensor."""
+    a pinned host tensor.  The whole batch moves together (so batched paths
+    such as the fan-beam kernels apply); views are chunked by bytes."""
     torch = _torch()
     dev = plan.device
     B = int(host.shape[0])
     nv, nr, nc = plan.sino_shape
-    view_bytes = nr * nc * 4
+    view_bytes = B * nr * nc * 4
     ranges = view_chunks(nv, view_bytes, chunk_bytes)
     plans = chunk_plans(plan, ranges)
     compute = torch.cuda.current_stream(dev)
@@ -75,30 +76,30 @@ def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CH
         if direction == 0:
             out = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, pin_memory=True)
             xd = src.to(dev, non_blocking=True)
-            for b in range(B):
-                pending = []
-                for (a, e), p in zip(ranges, plans):
-                    yd = p.forward(xd[b:b + 1])
-                    ev = torch.cuda.Event()
-                    ev.record(compute)
-                    copy.wait_event(ev)
-                    with torch.cuda.stream(copy):
-                        out[b, a:e].copy_(yd[0], non_blocking=True)
-                        yd.record_stream(copy)
-                    pending.append(yd)
+            for (a, e), p in zip(ranges, plans):
+                yd = p.forward(xd)
+                ev = torch.cuda.Event()
+                ev.record(compute)
+                copy.wait_event(ev)
+                with torch.cuda.stream(copy):
+                    if len(ranges) == 1:
+                        out.copy_(yd, non_blocking=True)
+                    else:
+                        out[:, a:e].copy_(yd, non_blocking=True)
+                    yd.record_stream(copy)
             compute.wait_stream(copy)
             compute.synchronize()
             return out
         out_d = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, device=dev)
-        for b in range(B):
-            for k, ((a, e), p) in enumerate(zip(ranges, plans)):
-                with torch.cuda.stream(copy):
-                    yd = src[b:b + 1, a:e].to(dev, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-                compute.wait_event(ev)
-                yd.record_stream(compute)
-                p.back(yd, out=out_d[b:b + 1], accumulate=k > 0)
+        for k, ((a, e), p) in enumerate(zip(ranges, plans)):
+            with torch.cuda.stream(copy):
+                part = src if len(ranges) == 1 else src[:, a:e]
+                yd = part.to(dev, non_blocking=True).contiguous()
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            compute.wait_event(ev)
+            yd.record_stream(compute)
+            p.back(yd, out=out_d, accumulate=k > 0)
         out = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, pin_memory=True)
         out.copy_(out_d, non_blocking=True)
         compute.synchronize()

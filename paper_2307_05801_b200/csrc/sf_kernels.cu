@@ -32,6 +32,9 @@
 #ifndef CTP_BK_MINB
 #define CTP_BK_MINB 4  // resident CTAs/SM the back kernel is register-budgeted for
 #endif
+#ifndef CTP_BK_QUNROLL
+#define CTP_BK_QUNROLL 1  // row-sum loop unroll (loads in flight per lane)
+#endif
 #ifndef CTP_FW_MINB
 #define CTP_FW_MINB 3
 #endif
@@ -94,6 +97,7 @@ constexpr int BK_ZPL = 8;           // voxels per lane
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
 constexpr int BK_QMAX = 480;        // per-warp row-sum table (rows): ZC * 1.8 + margin
 constexpr int BK_NCF = 4;           // footprint columns handled by the table path
+constexpr int BK_QUNROLL = CTP_BK_QUNROLL;  // row-sum loop unroll
 
 struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
   float A, B, E, lxy;
@@ -292,6 +296,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           const float2 T0 = bc2_(ef.ts[0]), T1 = bc2_(ef.ts[1]), T2 = bc2_(ef.ts[2]), T3 = bc2_(ef.ts[3]);
           const int n4 = (pk >> 4) & 0xfff;
           float4* q4 = reinterpret_cast<float4*>(qw);
+#pragma unroll BK_QUNROLL
           for (int t = lane; t < n4; t += 32) {
             const float4 a = __ldg(v0 + t), bq = __ldg(v1 + t), cq = __ldg(v2 + t), d = __ldg(v3 + t);
             float2 lo = mul2_(T0, make_float2(a.x, a.y));
