@@ -406,7 +406,10 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 // ---------------------------------------------------------------------------
 // forward projection: y = A x
 // ---------------------------------------------------------------------------
-constexpr int FW_CW = 8;                        // detector columns per tile
+#ifndef CTP_FW_CW
+#define CTP_FW_CW 8
+#endif
+constexpr int FW_CW = CTP_FW_CW;                     // detector columns per tile
 #ifndef CTP_FW_KR
 #define CTP_FW_KR 6
 #endif
@@ -426,7 +429,7 @@ struct FwEntry {
   int pad;
   float ts[FW_CW];  // weights of the tile's columns (0 outside the footprint)
 };
-static_assert(sizeof(FwEntry) == 80, "FwEntry layout");
+static_assert(sizeof(FwEntry) == 48 + 4 * FW_CW, "FwEntry layout");
 
 
 __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams& gp, int c0, int cw,
@@ -548,7 +551,10 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
 // candidates up lane-parallel (one per lane), compacts the surviving
 // (sub-)footprints into its private entry buffer, and gathers them into its
 // register tile.  No CTA barriers: warps of a CTA never wait for each other.
-constexpr int FV_WARPS = 4;
+#ifndef CTP_FV_WARPS
+#define CTP_FV_WARPS 4
+#endif
+constexpr int FV_WARPS = CTP_FV_WARPS;
 constexpr int FV_EBUF = 96;  // >= 31 pending + 64 from one setup round
 
 constexpr int FW_PADR = 8;  // garbage row slots on each side of the row buffer
