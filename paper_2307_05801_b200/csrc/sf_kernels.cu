@@ -236,6 +236,34 @@ __device__ __forceinline__ void back_slices(float (&acc)[BK_ZPL], const BkEntry&
   }
 }
 
+// Q(r) for 4 consecutive rows per lane and iteration (16-byte loads) over the
+// NC footprint columns: Q = ((t0 y0 + t1 y1) + ...) in fixed column order
+template <int NC>
+__device__ __forceinline__ void row_sums(float4* q4, const float* yv, int nr, const float (&ts)[BK_NCF],
+                                         int n4, int lane) {
+  const float4* v[NC];
+  float2 T[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    v[k] = reinterpret_cast<const float4*>(yv + k * nr);
+    T[k] = bc2_(ts[k]);
+  }
+#pragma unroll 1
+  for (int t = lane; t < n4; t += 32) {
+    float4 a[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) a[k] = __ldg(v[k] + t);
+    float2 lo = mul2_(T[0], make_float2(a[0].x, a[0].y));
+    float2 hi = mul2_(T[0], make_float2(a[0].z, a[0].w));
+#pragma unroll
+    for (int k = 1; k < NC; ++k) {
+      lo = fma2_(T[k], make_float2(a[k].x, a[k].y), lo);
+      hi = fma2_(T[k], make_float2(a[k].z, a[k].w), hi);
+    }
+    q4[t] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
+}
+
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
     float* __restrict__ out, int accumulate) {
@@ -289,25 +317,13 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
         if (pk & 1) {
           // fast path: everything precomputed; 4-row float4 row sums, then slices
           const float* yv = yb + (size_t)(vb + j) * view_elems + ef.off0;
-          const float4* v0 = reinterpret_cast<const float4*>(yv);
-          const float4* v1 = reinterpret_cast<const float4*>(yv + nr);
-          const float4* v2 = reinterpret_cast<const float4*>(yv + 2 * nr);
-          const float4* v3 = reinterpret_cast<const float4*>(yv + 3 * nr);
-          const float2 T0 = bc2_(ef.ts[0]), T1 = bc2_(ef.ts[1]), T2 = bc2_(ef.ts[2]), T3 = bc2_(ef.ts[3]);
           const int n4 = (pk >> 4) & 0xfff;
           float4* q4 = reinterpret_cast<float4*>(qw);
-#pragma unroll BK_QUNROLL
-          for (int t = lane; t < n4; t += 32) {
-            const float4 a = __ldg(v0 + t), bq = __ldg(v1 + t), cq = __ldg(v2 + t), d = __ldg(v3 + t);
-            float2 lo = mul2_(T0, make_float2(a.x, a.y));
-            float2 hi = mul2_(T0, make_float2(a.z, a.w));
-            lo = fma2_(T1, make_float2(bq.x, bq.y), lo);
-            hi = fma2_(T1, make_float2(bq.z, bq.w), hi);
-            lo = fma2_(T2, make_float2(cq.x, cq.y), lo);
-            hi = fma2_(T2, make_float2(cq.z, cq.w), hi);
-            lo = fma2_(T3, make_float2(d.x, d.y), lo);
-            hi = fma2_(T3, make_float2(d.z, d.w), hi);
-            q4[t] = make_float4(lo.x, lo.y, hi.x, hi.y);
+          switch (ef.ncol) {  // warp-uniform: load only the footprint's columns
+            case 1: row_sums<1>(q4, yv, nr, ef.ts, n4, lane); break;
+            case 2: row_sums<2>(q4, yv, nr, ef.ts, n4, lane); break;
+            case 3: row_sums<3>(q4, yv, nr, ef.ts, n4, lane); break;
+            default: row_sums<4>(q4, yv, nr, ef.ts, n4, lane); break;
           }
           __syncwarp();
           const int K = (pk >> 1) & 7, ra4 = pk >> 16;
