@@ -38,15 +38,6 @@
 #ifndef CTP_FW_MINB
 #define CTP_FW_MINB 3
 #endif
-#ifndef CTP_FW_GSKIP
-#define CTP_FW_GSKIP 0  // skip 32-row groups outside a column's row span
-#endif
-#ifndef CTP_FW_SCATTER
-#define CTP_FW_SCATTER 0  // forward phase 2 as conflict-free row scatter (else gather)
-#endif
-#ifndef CTP_FW_APPLY2
-#define CTP_FW_APPLY2 1  // packed f32x2 column apply
-#endif
 
 namespace ctp {
 
@@ -425,28 +416,30 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 #ifndef CTP_FW_CW
 #define CTP_FW_CW 8
 #endif
-constexpr int FW_CW = CTP_FW_CW;                     // detector columns per tile
+constexpr int FW_CW = CTP_FW_CW;  // detector columns per tile
 #ifndef CTP_FW_KR
 #define CTP_FW_KR 6
 #endif
-constexpr int FW_KR = CTP_FW_KR;                // 32-row groups per warp
-constexpr int FW_ROWS = 32 * FW_KR;             // rows per warp task
-constexpr int FW_PAD = 6;                       // zero sentinels on each side of a piece
-constexpr int FW_VBUF = 32 * FW_KR + 96;        // slices staged per warp and piece
-constexpr int FW_SBUF = FW_VBUF + 2 * FW_PAD;
+constexpr int FW_KR = CTP_FW_KR;     // 32-row groups per warp
+constexpr int FW_ROWS = 32 * FW_KR;  // rows per warp task
+constexpr int FW_XPAD = 4;           // zero slots below the staged slices
+// slices staged per entry (fast path) or per piece (generic path): the band's
+// rows plus slack for B < 1, rounded to whole 128-slice vector loads
+constexpr int FW_XCAP = ((32 * FW_KR + 64) + 127) / 128 * 128;
+constexpr int FW_XLEN = FW_XPAD + FW_XCAP + 4;  // + zero slots above
+constexpr int FW_NLD = FW_XCAP / 128;           // float4 x loads per lane (fast path)
 
 struct FwEntry {
-  int col;    // iy*nx + ix
-  int cinfo;  // first tile column offset | (count << 8)
+  int col;   // iy*nx + ix
+  int za4;   // first staged slice (a multiple of 4 on the vector path)
+  int nst;   // staged slices: za4 .. za4 + nst - 1 (0: the entry misses the band)
+  int info;  // g0 | g1 << 4 | ncand << 8 | fast << 15 (band-specific, see band_info)
   float A, B, E;
   float lxy, a0, a1;
-  float invB, cb;  // candidate slices of row r start at floor(r*invB + cb) + 1
-  int ncand;       // candidate slices per row (covers every nonzero overlap)
-  int pad;
+  float invB, cb;   // candidate slices of row r start at floor(r*invB + cb) + 1
   float ts[FW_CW];  // weights of the tile's columns (0 outside the footprint)
 };
 static_assert(sizeof(FwEntry) == 48 + 4 * FW_CW, "FwEntry layout");
-
 
 __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams& gp, int c0, int cw,
                                              float band_lo, float band_hi) {
@@ -456,17 +449,22 @@ __device__ __forceinline__ bool reaches_tile(const SubFoot& f, const GridParams&
   return cols_ok && thi > band_lo && tlo < band_hi;
 }
 
+// Candidate slices per row.  Slice iz overlaps row r only if iz lies in the
+// open interval ((r - .5 - E - A)/B, (r + .5 + E - A)/B) of length
+// L = (1 + 2E)/B; the candidates floor(s - 0.01) + 1 ... + ceil(L + 0.02) cover
+// it (an open interval of length L holds at most ceil(L) integers; the 0.01 /
+// 0.02 margins absorb fp32 rounding of lo / hi and of the interval ends).
+__device__ __forceinline__ int cand_count(float E, float invB) {
+  return (int)ceilf((1.0f + 2.0f * E) * invB + 0.02f);
+}
+
 __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int col, int c0, int cw) {
   e.col = col;
   e.A = f.A; e.B = f.B; e.E = f.E;
   e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
-  // slice iz overlaps row r only if iz lies in the open interval
-  // ((r - .5 - E - A)/B, (r + .5 + E - A)/B) of length 1/B + 1; the 0.01 /
-  // 0.02 margins absorb fp32 rounding of lo/hi and of the interval ends
   const float invB = 1.0f / f.B;
   e.invB = invB;
   e.cb = (-0.5f - f.E - f.A) * invB - 0.01f;
-  e.ncand = (int)ceilf((1.0f + 2.0f * f.E) * invB + 0.02f) + 1;
   const Trap p = make_trap(f);
   float ts[FW_CW];
   col_weights<FW_CW>(p, c0, ts);
@@ -476,52 +474,73 @@ __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int co
     const int cc = c0 + c;
     e.ts[c] = (cc >= lo && cc <= hi) ? ts[c] : 0.0f;
   }
-  e.cinfo = (lo - c0) | ((hi - lo + 1) << 8);  // informational
+  e.za4 = 0;
+  e.nst = 0;
+  e.info = 0;
 }
 
-// P(r) += sum over NC candidate slices of tt(r, iz) * amp x  (sentinels add 0).
-// max(0, min(hi, r+.5) - max(lo, r-.5)) equals clamp(r+.5,lo,hi) -
-// clamp(r-.5,lo,hi) bit for bit (same operands when the intervals overlap,
-// exactly 0 otherwise), one instruction shorter.
-template <int NC>
-__device__ __forceinline__ float gather_slices(float p, const float4* sb, int i0, float rlo,
-                                               float rhi) {
-#pragma unroll
-  for (int i = 0; i < NC; ++i) {
-    const float4 d = sb[i0 + i];
-    p = fma_(fmaxf(sub_(fminf(rhi, d.y), fmaxf(rlo, d.x)), 0.0f), d.z, p);
-  }
-  return p;
+// Band-specific part of an entry, evaluated by the lane that set the entry up:
+// the slices za..zb that can reach rows [rw0, rw1], the staged range (za
+// rounded down to a multiple of 4 for 16-byte loads), the 32-row groups the
+// column's rows fall into, and whether the fast path applies.
+__device__ __forceinline__ void band_info(FwEntry& e, const GridParams& gp, int rw0, int rw1, bool vec) {
+  const int nc = cand_count(e.E, e.invB);
+  const int za = max((int)floorf(fmaf((float)rw0, e.invB, e.cb)) + 1, 0);
+  const int zb = min((int)floorf(fmaf((float)rw1, e.invB, e.cb)) + nc, gp.nz - 1);
+  const int za4 = vec ? (za & ~3) : za;
+  // rows reached by slices za..zb: [T(za) - E, T(zb) + E], widened by a row
+  const float tlo = sub_(fma_(e.B, (float)za, e.A), e.E);
+  const float thi = add_(fma_(e.B, (float)zb, e.A), e.E);
+  const int r_lo = max((int)floorf(tlo) - 1, rw0), r_hi = min((int)ceilf(thi) + 1, rw1);
+  const bool empty = za > zb || r_lo > r_hi;
+  e.za4 = za4;
+  e.nst = empty ? 0 : zb - za4 + 1;
+  const int g0 = (r_lo - rw0) >> 5, g1 = (r_hi - rw0) >> 5;
+  const bool fast = !empty && e.nst <= FW_XCAP && nc <= 3;
+  e.info = empty ? 0 : (g0 | (g1 << 4) | (min(nc, 127) << 8) | (fast ? (1 << 15) : 0));
 }
 
-// rows of the 32-row groups [g0, g1] of this warp: P(r) = sum over NC candidate
-// slices; then y(r, c) += ts(c) P(r) for all tile columns (ts = 0 where the
-// footprint ends), two columns per packed FFMA2
+// Rows of this lane in the 32-row groups [g0, g1]: P(r) = sum over NC
+// candidate slices j of tt(r, j) * xa(j), with T_j = A + B j recomputed in
+// registers (the same fma as the back kernel, so lo/hi are bitwise equal) and
+// only xa = amp * x staged in shared memory; then y(r, c) += ts(c) P(r).
+// tt = max(0, min(hi, r+.5) - max(lo, r-.5)) equals the back kernel's
+// clamp(r+.5,lo,hi) - clamp(r-.5,lo,hi) bit for bit.  Candidates outside the
+// staged range read zero slots (idx is clamped to [0, hic]; both ends of the
+// buffer hold >= 4 zeros, and a clamp only happens for virtual slices j < 0 or
+// j >= nz, whose xa is 0).
 template <int NC>
 __device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
-                                        const float4* sw, int rw0, int lane, float invB, float cb,
-                                        int base, int lim, int g0, int g1) {
+                                        const float* xs, float rbase, float A, float B, float E,
+                                        float invB, float cb, int off, int hic, int g0, int g1) {
 #pragma unroll
   for (int kk = 0; kk < FW_KR; ++kk) {
-#if CTP_FW_GSKIP
     if (kk < g0 || kk > g1) continue;  // warp-uniform
-#endif
-    const float rf = (float)(rw0 + 32 * kk + lane);
-    const int c = (int)floorf(fmaf(rf, invB, cb)) + base;
-    const int i0 = min(max(c, 0), lim);
-    const float p = gather_slices<NC>(0.0f, sw, i0, sub_(rf, 0.5f), add_(rf, 0.5f));
-#if CTP_FW_APPLY2
-    const float2 pp = bc2_(p);
+    const float rf = rbase + (float)(32 * kk);
+    const float cf = floorf(fmaf(rf, invB, cb));  // first candidate - 1
+    const int idx = min(max((int)cf + off, 0), hic);
+    const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
+    const float j0 = add_(cf, 1.0f);
+    const float2 T = fma2_(bc2_(B), make_float2(j0, add_(j0, 1.0f)), bc2_(A));
+    const float2 lo = add2_(T, bc2_(-E)), hi = add2_(T, bc2_(E));
+    float2 ov = add2_(make_float2(fminf(hi.x, rhi), fminf(hi.y, rhi)),
+                      make_float2(-fmaxf(lo.x, rlo), -fmaxf(lo.y, rlo)));
+    ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
+    const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
+    float p = add_(pp.x, pp.y);
+    if (NC == 3) {
+      const float T2 = fma_(B, add_(j0, 2.0f), A);
+      const float lo2 = add_(T2, -E), hi2 = add_(T2, E);
+      const float o2 = fmaxf(sub_(fminf(hi2, rhi), fmaxf(lo2, rlo)), 0.0f);
+      p = fma_(o2, xs[idx + 2], p);
+    }
+    const float2 p2 = bc2_(p);
 #pragma unroll
     for (int cc = 0; cc < FW_CW; cc += 2) {
-      const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), pp, make_float2(acc[kk][cc], acc[kk][cc + 1]));
+      const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), p2, make_float2(acc[kk][cc], acc[kk][cc + 1]));
       acc[kk][cc] = a.x;
       acc[kk][cc + 1] = a.y;
     }
-#else
-#pragma unroll
-    for (int cc = 0; cc < FW_CW; ++cc) acc[kk][cc] = fma_(ts[cc], p, acc[kk][cc]);
-#endif
   }
 }
 
@@ -564,20 +583,19 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
 // One WARP owns one task = (view, FW_CW-column tile, FW_KR*32-row band).  It
 // enumerates the wedge of voxel columns reaching its tile (rows of primary
 // indices in chunks of 32, counts prefix-scanned with shuffles), sets the
-// candidates up lane-parallel (one per lane), compacts the surviving
-// (sub-)footprints into its private entry buffer, and gathers them into its
-// register tile.  No CTA barriers: warps of a CTA never wait for each other.
+// candidates up lane-parallel (one per lane, including everything the
+// per-entry loop needs for this band), compacts the surviving (sub-)footprints
+// into its private entry buffer, and gathers them into its register tile.  No
+// CTA barriers: warps of a CTA never wait for each other.
 #ifndef CTP_FV_WARPS
 #define CTP_FV_WARPS 4
 #endif
 constexpr int FV_WARPS = CTP_FV_WARPS;
 constexpr int FV_EBUF = 96;  // >= 31 pending + 64 from one setup round
 
-constexpr int FW_PADR = 8;  // garbage row slots on each side of the row buffer
 struct FvSmem {
   FwEntry ent[FV_EBUF];
-  float4 sbuf[FW_SBUF];
-  float prow[FW_ROWS + 2 * FW_PADR];  // per-row partial sums P(r) of one entry
+  float xs[FW_XLEN];  // staged amp * x of one entry (or one piece)
 };
 
 size_t forward_warp_smem_bytes() { return sizeof(FvSmem) * FV_WARPS; }
@@ -591,205 +609,111 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// slice range of entry E that can reach rows [rw0, rw1]
-__device__ __forceinline__ void fw_range(const FwEntry& E, float rw0f, float rw1f, int nz, int& za,
-                                         int& zb) {
-  za = max((int)floorf(fmaf(rw0f, E.invB, E.cb)) + 1, 0);
-  zb = min((int)floorf(fmaf(rw1f, E.invB, E.cb)) + E.ncand, nz - 1);
-}
-
-constexpr int FW_NPF = (FW_VBUF + 31) / 32;  // prefetched x values per lane
-
-// issue the loads of x for slices za.. (at most FW_VBUF) of one voxel column
-__device__ __forceinline__ void fw_prefetch(float (&xr)[FW_NPF], const float* __restrict__ xc, int za,
-                                            int nvox, int lane) {
+// issue the loads of x for the staged slices of one entry (16-byte loads when
+// the column layout allows, slots >= nst read as 0)
+template <bool VEC>
+__device__ __forceinline__ void fw_prefetch(float4 (&xv)[FW_NLD], const float* __restrict__ xc, int nst,
+                                            int lane) {
 #pragma unroll
-  for (int t = 0; t < FW_NPF; ++t) {
-    const int i = lane + 32 * t;
-    xr[t] = i < nvox ? __ldg(xc + za + i) : 0.0f;
-  }
-}
-
-// Scatter path of one entry: lanes = slices.  Slice iz adds
-// c_k = tt_k * (amp x) to rows r0+k, k < K, with tt_k evaluated exactly as in
-// the back kernel (first boundary lo, last hi, middle ones clamped).  Targets
-// of one RMW step are distinct: r0 strictly increases with iz when B > 1.001;
-// for 0.5005 < B <= 1.001 (PAIR) two neighbouring slices may share r0, and the
-// follower's coefficient is first added to the leader's (no triples occur).
-// Rows outside the warp's band go to garbage slots that are never read.
-template <int K, bool PAIR>
-__device__ __forceinline__ void fw_scatter(float* prow, const FwEntry& E, const float (&xr)[FW_NPF],
-                                           int za, int nvox, int rw0, int lane) {
-  const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
-  constexpr int LAST = FW_ROWS + 2 * FW_PADR - 1;
-#pragma unroll
-  for (int t = 0; t < FW_NPF; ++t) {
-    if (32 * t >= nvox) break;  // warp-uniform
-    const int i = lane + 32 * t;
-    const bool act = i < nvox;
-    const float izf = (float)(za + i);
-    const float T = fma_(B, izf, A);
-    const float lo = add_(T, -Eh), hi = add_(T, Eh);
-    const float q = fma_(a1, izf, a0);
-    const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-    const float xa = mul_(amp, xr[t]);
-    const float fl = floorf(add_(lo, -0.5f));
-    const int r0 = (int)fl + 1;
-    float c[K];
-    float g = lo;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const float gn = (k == K - 1) ? hi : clampf_(add_(fl, (float)k + 1.5f), lo, hi);
-      c[k] = mul_(add_(gn, -g), xa);
-      g = gn;
-    }
-    bool writer = act;
-    if (PAIR) {
-      const int r0p = __shfl_up_sync(0xffffffffu, r0, 1);
-      const int r0n = __shfl_down_sync(0xffffffffu, r0, 1);
-      const bool actn = __shfl_down_sync(0xffffffffu, act ? 1 : 0, 1) != 0;
-      const bool follower = lane > 0 && r0p == r0;   // leader (lane-1) takes our share
-      const bool leader = lane < 31 && actn && r0n == r0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const float cn = __shfl_down_sync(0xffffffffu, c[k], 1);
-        if (leader) c[k] = add_(c[k], cn);
-      }
-      writer = act && !follower;
-    }
-    const int base = writer ? r0 - rw0 + FW_PADR : 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int j = min(max(base + k, 0), LAST);
-      if (writer) prow[j] = add_(prow[j], c[k]);
-      __syncwarp();
+  for (int t = 0; t < FW_NLD; ++t) {
+    const int s = 4 * lane + 128 * t;
+    if (VEC) {
+      xv[t] = s < nst ? __ldg(reinterpret_cast<const float4*>(xc + s)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      xv[t].x = s < nst ? __ldg(xc + s) : 0.0f;
+      xv[t].y = s + 1 < nst ? __ldg(xc + s + 1) : 0.0f;
+      xv[t].z = s + 2 < nst ? __ldg(xc + s + 2) : 0.0f;
+      xv[t].w = s + 3 < nst ? __ldg(xc + s + 3) : 0.0f;
     }
   }
 }
 
+template <bool VEC>
 __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_KR][FW_CW],
                                            const GridParams& gp, const float* __restrict__ xb,
-                                           int rw0, int rw1, int lane) {
-  float4* sw = S.sbuf;
-  const float rw0f = (float)rw0, rw1f = (float)rw1;
+                                           int rw0, int lane) {
+  float* xs = S.xs;
+  const float rbase = (float)(rw0 + lane);
   // software pipeline: x of the next fast-path entry is in flight while the
   // current entry is gathered
-  float xr[FW_NPF];
-  int e_pf = 0;  // entry whose x is in xr (or nent if none)
+  float4 xv[FW_NLD];
   auto next_fast = [&](int e) {
     for (; e < nent; ++e) {
-      int za, zb;
-      fw_range(S.ent[e], rw0f, rw1f, gp.nz, za, zb);
-      if (za <= zb && zb - za + 1 <= FW_VBUF && S.ent[e].ncand <= 6) {
-        fw_prefetch(xr, xb + (size_t)S.ent[e].col * gp.nz, za, zb - za + 1, lane);
+      if (S.ent[e].info & (1 << 15)) {
+        fw_prefetch<VEC>(xv, xb + (size_t)S.ent[e].col * gp.nz + S.ent[e].za4, S.ent[e].nst, lane);
         return e;
       }
     }
     return nent;
   };
-  e_pf = next_fast(0);
+  int e_pf = next_fast(0);
   for (int e = 0; e < nent; ++e) {
     const FwEntry& E = S.ent[e];
-    const float invB = E.invB, cb = E.cb;
-    const int nc = E.ncand;
-    int za, zb;
-    fw_range(E, rw0f, rw1f, gp.nz, za, zb);
-    if (za > zb) continue;
+    const int info = E.info;
+    const int nst = E.nst;
+    if (nst == 0) continue;
     const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
-    const float* xc = xb + (size_t)E.col * gp.nz;
+    const float invB = E.invB, cb = E.cb;
+    const int za4 = E.za4;
+    const int g0 = info & 15, g1 = (info >> 4) & 15, nc = (info >> 8) & 127;
     float ts[FW_CW];
 #pragma unroll
     for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
-    const int nvox_all = zb - za + 1;
-    const int K = rows_per_slice(B);
-    int mode = 0;  // 0: gather path
-#if CTP_FW_SCATTER
-    if (B > 1.001f) mode = K == 3 ? 1 : (K == 4 ? 2 : 0);
-    else if (B > 0.5005f) mode = K == 2 ? 3 : (K == 3 ? 4 : 0);
-#endif
-    if (e == e_pf && mode != 0) {
-      switch (mode) {
-        case 1: fw_scatter<3, false>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
-        case 2: fw_scatter<4, false>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
-        case 3: fw_scatter<2, true>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
-        default: fw_scatter<3, true>(S.prow, E, xr, za, nvox_all, rw0, lane); break;
-      }
-      e_pf = next_fast(e + 1);  // loads for the next entry overlap the apply
-      // y(r, c) += ts(c) P(r); reset P
-#pragma unroll
-      for (int kk = 0; kk < FW_KR; ++kk) {
-        float* pr = S.prow + FW_PADR + 32 * kk + lane;
-        const float p = *pr;
-        *pr = 0.0f;
-        const float2 pp = bc2_(p);
-#pragma unroll
-        for (int cc = 0; cc < FW_CW; cc += 2) {
-          const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), pp, make_float2(acc[kk][cc], acc[kk][cc + 1]));
-          acc[kk][cc] = a.x;
-          acc[kk][cc + 1] = a.y;
-        }
-      }
-      __syncwarp();
-      continue;
-    }
     if (e == e_pf) {
-      // stage (lo, hi, amp*x) of slices za..zb between zero sentinels
-      // two 32-slice chunks per step in packed f32x2 (same IEEE ops as scalar)
+      // stage xa = amp * x of slices za4 .. za4 + nst - 1 (4 per lane and load)
 #pragma unroll
-      for (int t = 0; t < FW_NPF; t += 2) {
-        const int i = lane + 32 * t;
-        if (32 * t >= nvox_all) break;  // warp-uniform
-        const float2 izf = make_float2((float)(za + i), (float)(za + i + 32));
-        const float2 T = fma2_(bc2_(B), izf, bc2_(A));
-        const float2 q = fma2_(bc2_(a1), izf, bc2_(a0));
-        const float2 tq = fma2_(q, q, bc2_(1.0f));
-        const float2 amp = mul2_(bc2_(lxy), make_float2(sqrt_approx(tq.x), sqrt_approx(tq.y)));
-        const float2 lo = add2_(T, bc2_(-Eh)), hi = add2_(T, bc2_(Eh));
-        const float2 xa = mul2_(amp, make_float2(xr[t], t + 1 < FW_NPF ? xr[t + 1] : 0.0f));
-        if (i < nvox_all) sw[FW_PAD + i] = make_float4(lo.x, hi.x, xa.x, 0.0f);
-        if (i + 32 < nvox_all) sw[FW_PAD + i + 32] = make_float4(lo.y, hi.y, xa.y, 0.0f);
+      for (int t = 0; t < FW_NLD; ++t) {
+        const int s = 4 * lane + 128 * t;
+        if (128 * t >= nst) break;  // warp-uniform
+        const float z0 = (float)(za4 + s);
+        const float2 izA = make_float2(z0, add_(z0, 1.0f)), izB = make_float2(add_(z0, 2.0f), add_(z0, 3.0f));
+        const float2 qA = fma2_(bc2_(a1), izA, bc2_(a0)), qB = fma2_(bc2_(a1), izB, bc2_(a0));
+        const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
+        const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
+        const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
+        const float2 xaA = mul2_(ampA, make_float2(xv[t].x, xv[t].y));
+        const float2 xaB = mul2_(ampB, make_float2(xv[t].z, xv[t].w));
+        if (s < nst) *reinterpret_cast<float4*>(xs + FW_XPAD + s) = make_float4(xaA.x, xaA.y, xaB.x, xaB.y);
       }
-      if (lane < FW_PAD) sw[FW_PAD + nvox_all + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
+      if (lane < 4) xs[FW_XPAD + ((nst + 3) & ~3) + lane] = 0.0f;
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this gather
-      const int base = 1 - za + FW_PAD, lim = FW_PAD + nvox_all;
-      // 32-row groups touched by the column: rows [T(0) - E, T(nz-1) + E]
-      const float tlo = sub_(fma_(B, 0.0f, A), Eh), thi = add_(fma_(B, (float)(gp.nz - 1), A), Eh);
-      const int g0 = max(0, ((int)floorf(tlo) - 1 - rw0) >> 5);
-      const int g1 = min(FW_KR - 1, ((int)ceilf(thi) + 1 - rw0) >> 5);
-      if (nc <= 2) fw_rows<2>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
-      else if (nc == 3) fw_rows<3>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
-      else if (nc == 4) fw_rows<4>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
-      else fw_rows<6>(acc, ts, sw, rw0, lane, invB, cb, base, lim, g0, g1);
+      const int off = 1 - za4 + FW_XPAD, hic = FW_XPAD + nst;
+      if (nc <= 2) fw_rows<2>(acc, ts, xs, rbase, A, B, Eh, invB, cb, off, hic, g0, g1);
+      else fw_rows<3>(acc, ts, xs, rbase, A, B, Eh, invB, cb, off, hic, g0, g1);
       __syncwarp();
       continue;
     }
-    // generic: several pieces and/or many candidates per row
+    // generic path: many candidates per row and/or more slices than one
+    // staging buffer holds; pieces of FW_XCAP slices, exact candidate loops
+    const int za = max((int)floorf(fmaf((float)rw0, invB, cb)) + 1, 0);
+    const int zb = za4 + nst - 1;
     float P[FW_KR];
 #pragma unroll
     for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
-    for (int piece = za; piece <= zb; piece += FW_VBUF) {
-      const int pe = min(piece + FW_VBUF - 1, zb);
-      const int nvox = pe - piece + 1;
-      for (int i = lane; i < nvox; i += 32) {
+    const float* xc = xb + (size_t)E.col * gp.nz;
+    for (int piece = za; piece <= zb; piece += FW_XCAP) {
+      const int pe = min(piece + FW_XCAP - 1, zb);
+      const int n = pe - piece + 1;
+      for (int i = lane; i < n; i += 32) {
         const float izf = (float)(piece + i);
-        const float T = fma_(B, izf, A);
         const float q = fma_(a1, izf, a0);
         const float amp = mul_(lxy, sqrt_approx(fma_(q, q, 1.0f)));
-        sw[FW_PAD + i] = make_float4(sub_(T, Eh), add_(T, Eh), mul_(amp, __ldg(xc + piece + i)), 0.0f);
+        xs[FW_XPAD + i] = mul_(amp, __ldg(xc + piece + i));
       }
-      if (lane < FW_PAD) sw[FW_PAD + nvox + lane] = make_float4(3e38f, 3e38f, 0.0f, 0.0f);
       __syncwarp();
 #pragma unroll
       for (int kk = 0; kk < FW_KR; ++kk) {
-        const float rf = (float)(rw0 + 32 * kk + lane);
+        if (kk < g0 || kk > g1) continue;
+        const float rf = rbase + (float)(32 * kk);
         const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
-        const int c = (int)floorf(fmaf(rf, invB, cb)) + 1 - piece + FW_PAD;
-        const int j1 = min(c + nc - 1, FW_PAD + nvox - 1);
+        const int c = (int)floorf(fmaf(rf, invB, cb));
+        const int j1 = min(c + nc, pe);
         float p = P[kk];
-        for (int j = max(c, FW_PAD); j <= j1; ++j) {
-          const float4 d = sw[j];
-          p = fma_(fmaxf(sub_(fminf(rhi, d.y), fmaxf(rlo, d.x)), 0.0f), d.z, p);
+        for (int j = max(c + 1, piece); j <= j1; ++j) {
+          const float T = fma_(B, (float)j, A);
+          const float lo = add_(T, -Eh), hi = add_(T, Eh);
+          p = fma_(fmaxf(sub_(fminf(hi, rhi), fmaxf(lo, rlo)), 0.0f), xs[FW_XPAD + j - piece], p);
         }
         P[kk] = p;
       }
@@ -802,6 +726,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
   }
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
     GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xT,
     float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
@@ -847,8 +772,7 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
   for (int k = 0; k < FW_KR; ++k)
 #pragma unroll
     for (int c = 0; c < FW_CW; ++c) acc[k][c] = 0.0f;
-  if (lane < FW_PAD) S.sbuf[lane] = make_float4(-3e38f, -3e38f, 0.0f, 0.0f);  // lower sentinels
-  for (int j = lane; j < FW_ROWS + 2 * FW_PADR; j += 32) S.prow[j] = 0.0f;
+  if (lane < FW_XPAD) S.xs[lane] = 0.0f;  // zero slots below the staged slices
   __syncwarp();
   const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
 
@@ -899,18 +823,24 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
       const int n = __popc(mask);
       const int ni = warp_incl_scan(n, lane);
       const int off = pending + ni - n;
-      if (mask & 1) write_entry(S.ent[off], f0, col, c0, cw);
-      if (mask & 2) write_entry(S.ent[off + (mask & 1)], f1, col, c0, cw);
+      if (mask & 1) {
+        write_entry(S.ent[off], f0, col, c0, cw);
+        band_info(S.ent[off], gp, rw0, rw1, VEC);
+      }
+      if (mask & 2) {
+        write_entry(S.ent[off + (mask & 1)], f1, col, c0, cw);
+        band_info(S.ent[off + (mask & 1)], gp, rw0, rw1, VEC);
+      }
       pending += __shfl_sync(0xffffffffu, ni, 31);
       __syncwarp();
       if (pending >= 32) {
-        fw_process(S, pending, acc, gp, xb, rw0, rw1, lane);
+        fw_process<VEC>(S, pending, acc, gp, xb, rw0, lane);
         pending = 0;
         __syncwarp();
       }
     }
   }
-  if (pending > 0) fw_process(S, pending, acc, gp, xb, rw0, rw1, lane);
+  if (pending > 0) fw_process<VEC>(S, pending, acc, gp, xb, rw0, lane);
 
   // store the tile: y[b][v][r][c0 + c]
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
@@ -1193,8 +1123,10 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float
 cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const float* xT, float* sino,
                            int batch, bool accumulate, cudaStream_t st) {
   const size_t smem = forward_warp_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(sf_forward_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
+  const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
+  auto kern = vec ? sf_forward_kernel<true> : sf_forward_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long nbands = (gp.nr + FW_ROWS - 1) / FW_ROWS;
   const long long ntiles = (gp.nc + FW_CW - 1) / FW_CW;
@@ -1206,8 +1138,7 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
     const long long rem = ntasks - t0;
     const long long nb = (rem + FV_WARPS - 1) / FV_WARPS;
     const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
-    sf_forward_kernel<<<grid, FV_WARPS * 32, smem, st>>>(g2, vcoef, xT, sino, accumulate ? 1 : 0, t0,
-                                                         ntasks);
+    kern<<<grid, FV_WARPS * 32, smem, st>>>(g2, vcoef, xT, sino, accumulate ? 1 : 0, t0, ntasks);
   }
   return cudaGetLastError();
 }
