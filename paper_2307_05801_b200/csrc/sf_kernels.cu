@@ -36,7 +36,7 @@
 #define CTP_BK_QUNROLL 1  // row-sum loop unroll (loads in flight per lane)
 #endif
 #ifndef CTP_FW_MINB
-#define CTP_FW_MINB 3
+#define CTP_FW_MINB 4
 #endif
 
 namespace ctp {
@@ -255,8 +255,35 @@ __device__ __forceinline__ void row_sums(float4* q4, const float* yv, int nr, co
   }
 }
 
+// Lane-parallel footprint setup of one voxel column for views vb + lane: the
+// entries of this lane's view go to e[0] (and e[1] for a split voxel).
+// Returns whether any lane of the warp has a split voxel.  Out of line: it is
+// run once per 32 views, and keeping its register-hungry geometry out of the
+// per-view loop leaves that loop's registers alone.
+__device__ __noinline__ bool back_setup(const GridParams& gp, const ViewCoef* __restrict__ vcoef, int vb,
+                                        int ix, int iy, int izs, int ize, BkEntry* e) {
+  const int v = vb + (threadIdx.x & 31);
+  BkEntry e0, e1;
+  e0.ncol = 0;
+  e0.pk = 0;
+  e1.ncol = 0;
+  e1.pk = 0;
+  int mask = 0;
+  if (v < gp.nv) {
+    const ViewCoef vc = vcoef[v];
+    SubFoot f0, f1;
+    mask = column_footprint(vc, gp, ix, iy, f0, f1);
+    if (mask & 1) fill_entry(e0, f0, gp, izs, ize);
+    if (mask & 2) fill_entry(e1, f1, gp, izs, ize);
+  }
+  e[0] = e0;
+  const bool split = __any_sync(0xffffffffu, (mask & 2) != 0);
+  if (split) e[1] = e1;
+  return split;
+}
+
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
-    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
     float* __restrict__ out, int accumulate) {
   __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
   __shared__ __align__(16) float qbuf[BK_WARPS][BK_QMAX + 8];
@@ -283,26 +310,13 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 
   for (int vb = 0; vb < gp.nv; vb += 32) {
     // ---- lane-parallel footprint setup: lane l <- view vb + l
-    {
-      const int v = vb + lane;
-      BkEntry e0, e1;
-      e0.ncol = 0;
-      e1.ncol = 0;
-      if (v < gp.nv) {
-        const ViewCoef vc = vcoef[v];
-        SubFoot f0, f1;
-        const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if (mask & 1) fill_entry(e0, f0, gp, izs, ize);
-        if (mask & 2) fill_entry(e1, f1, gp, izs, ize);
-      }
-      my[lane][0] = e0;
-      my[lane][1] = e1;
-    }
+    // nsub = 2 when any view of this batch splits the voxel (_sf_subdivide), else 1
+    const int nsub = back_setup(gp, vcoef, vb, ix, iy, izs, ize, &my[lane][0]) ? 2 : 1;
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
     for (int j = 0; j < nvb; ++j) {
 #pragma unroll 1
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < nsub; ++s) {
         const BkEntry& ef = my[j][s];
         const int pk = ef.pk;
         if (pk & 1) {
@@ -325,8 +339,8 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           __syncwarp();
           continue;
         }
-        const BkEntry e = ef;
-        if (e.ncol == 0) continue;
+        if (ef.ncol == 0) continue;
+        const BkEntry& e = ef;  // (shared memory: no private copy on the rare paths)
         const int K = rows_per_slice(e.B);
         const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
         const int Rz = first_row(sub_(fma_(e.B, (float)ize, e.A), e.E)) + K - 1;
@@ -414,11 +428,11 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 // forward projection: y = A x
 // ---------------------------------------------------------------------------
 #ifndef CTP_FW_CW
-#define CTP_FW_CW 8
+#define CTP_FW_CW 4
 #endif
 constexpr int FW_CW = CTP_FW_CW;  // detector columns per tile
 #ifndef CTP_FW_KR
-#define CTP_FW_KR 6
+#define CTP_FW_KR 8
 #endif
 constexpr int FW_KR = CTP_FW_KR;     // 32-row groups per warp
 constexpr int FW_ROWS = 32 * FW_KR;  // rows per warp task
@@ -726,9 +740,53 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
   }
 }
 
+// Footprint setup of the wedge candidates k = cbase + lane (one per lane):
+// owner primary index by binary search over the exclusive scan, footprint of
+// the voxel column, test against the tile, compaction of the surviving
+// (sub-)footprints into ent[0..).  Returns how many entries the warp added.
+// Out of line: it holds most of the kernel's geometry, and keeping it out of
+// the gather loop's register allocation avoids rematerialisation there.
+__device__ __noinline__ int fw_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp, FwEntry* ent,
+                                          int k, int total, int ib, int excl, int jl, bool primary_x, int c0,
+                                          int cw, float band_lo, float band_hi, int rw0, int rw1, bool vec) {
+  const int lane = threadIdx.x & 31;
+  // owner lane o: the largest lane with excl_o <= k (it has cnt_o > 0)
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int ex = __shfl_sync(0xffffffffu, excl, o + step);
+    if (ex <= k) o += step;
+  }
+  const int jo = __shfl_sync(0xffffffffu, jl, o);
+  const int exo = __shfl_sync(0xffffffffu, excl, o);
+  SubFoot f0, f1;
+  int mask = 0, col = 0;
+  if (k < total) {
+    const ViewCoef vc = *vcp;
+    const int ii = ib + o, j = jo + (k - exo);
+    const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
+    col = iy * gp.nx + ix;
+    mask = column_footprint(vc, gp, ix, iy, f0, f1);
+    if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
+    if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
+  }
+  const int n = __popc(mask);
+  const int ni = warp_incl_scan(n, lane);
+  const int off = ni - n;
+  if (mask & 1) {
+    write_entry(ent[off], f0, col, c0, cw);
+    band_info(ent[off], gp, rw0, rw1, vec);
+  }
+  if (mask & 2) {
+    write_entry(ent[off + (mask & 1)], f1, col, c0, cw);
+    band_info(ent[off + (mask & 1)], gp, rw0, rw1, vec);
+  }
+  return __shfl_sync(0xffffffffu, ni, 31);
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
-    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xT,
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xT,
     float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -800,38 +858,8 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
     const int excl = incl - cnt;
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
-      const int k = cbase + lane;
-      // owner lane o: the largest lane with excl_o <= k (it has cnt_o > 0)
-      int o = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int ex = __shfl_sync(0xffffffffu, excl, o + step);
-        if (ex <= k) o += step;
-      }
-      const int jo = __shfl_sync(0xffffffffu, jl, o);
-      const int exo = __shfl_sync(0xffffffffu, excl, o);
-      SubFoot f0, f1;
-      int mask = 0, col = 0;
-      if (k < total) {
-        const int ii = ib + o, j = jo + (k - exo);
-        const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
-        col = iy * gp.nx + ix;
-        mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
-        if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
-      }
-      const int n = __popc(mask);
-      const int ni = warp_incl_scan(n, lane);
-      const int off = pending + ni - n;
-      if (mask & 1) {
-        write_entry(S.ent[off], f0, col, c0, cw);
-        band_info(S.ent[off], gp, rw0, rw1, VEC);
-      }
-      if (mask & 2) {
-        write_entry(S.ent[off + (mask & 1)], f1, col, c0, cw);
-        band_info(S.ent[off + (mask & 1)], gp, rw0, rw1, VEC);
-      }
-      pending += __shfl_sync(0xffffffffu, ni, 31);
+      pending += fw_candidates(gp, vcoef + v, S.ent + pending, cbase + lane, total, ib, excl, jl, primary_x,
+                               c0, cw, band_lo, band_hi, rw0, rw1, VEC);
       __syncwarp();
       if (pending >= 32) {
         fw_process<VEC>(S, pending, acc, gp, xb, rw0, lane);
