@@ -36,7 +36,7 @@
 #define CTP_BK_QUNROLL 1  // row-sum loop unroll (loads in flight per lane)
 #endif
 #ifndef CTP_FW_MINB
-#define CTP_FW_MINB 4
+#define CTP_FW_MINB 3
 #endif
 
 namespace ctp {
@@ -432,10 +432,11 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
 #endif
 constexpr int FW_CW = CTP_FW_CW;  // detector columns per tile
 #ifndef CTP_FW_KR
-#define CTP_FW_KR 8
+#define CTP_FW_KR 12
 #endif
 constexpr int FW_KR = CTP_FW_KR;     // 32-row groups per warp
 constexpr int FW_ROWS = 32 * FW_KR;  // rows per warp task
+static_assert(FW_KR <= 32, "row groups are 5-bit in FwEntry::info");
 constexpr int FW_XPAD = 4;           // zero slots below the staged slices
 // slices staged per entry (fast path) or per piece (generic path): the band's
 // rows plus slack for B < 1, rounded to whole 128-slice vector loads
@@ -444,10 +445,10 @@ constexpr int FW_XLEN = FW_XPAD + FW_XCAP + 4;  // + zero slots above
 constexpr int FW_NLD = FW_XCAP / 128;           // float4 x loads per lane (fast path)
 
 struct FwEntry {
-  int col;   // iy*nx + ix
+  int col;   // iy*nx + ix; band_info turns it into the x offset col*nz + za4 of the first staged slice
   int za4;   // first staged slice (a multiple of 4 on the vector path)
   int nst;   // staged slices: za4 .. za4 + nst - 1 (0: the entry misses the band)
-  int info;  // g0 | g1 << 4 | ncand << 8 | fast << 15 (band-specific, see band_info)
+  int info;  // g0 | g1 << 5 | ncand << 10 | fast << 17 (band-specific, see band_info)
   float A, B, E;
   float lxy, a0, a1;
   float invB, cb;   // candidate slices of row r start at floor(r*invB + cb) + 1
@@ -509,51 +510,74 @@ __device__ __forceinline__ void band_info(FwEntry& e, const GridParams& gp, int 
   const bool empty = za > zb || r_lo > r_hi;
   e.za4 = za4;
   e.nst = empty ? 0 : zb - za4 + 1;
+  e.col = e.col * gp.nz + za4;  // 32-bit: the launcher checks nx*ny*nz < 2^31
   const int g0 = (r_lo - rw0) >> 5, g1 = (r_hi - rw0) >> 5;
   const bool fast = !empty && e.nst <= FW_XCAP && nc <= 3;
-  e.info = empty ? 0 : (g0 | (g1 << 4) | (min(nc, 127) << 8) | (fast ? (1 << 15) : 0));
+  e.info = empty ? 0 : (g0 | (g1 << 5) | (min(nc, 127) << 10) | (fast ? (1 << 17) : 0));
 }
 
-// Rows of this lane in the 32-row groups [g0, g1]: P(r) = sum over NC
-// candidate slices j of tt(r, j) * xa(j), with T_j = A + B j recomputed in
-// registers (the same fma as the back kernel, so lo/hi are bitwise equal) and
-// only xa = amp * x staged in shared memory; then y(r, c) += ts(c) P(r).
-// tt = max(0, min(hi, r+.5) - max(lo, r-.5)) equals the back kernel's
-// clamp(r+.5,lo,hi) - clamp(r-.5,lo,hi) bit for bit.  Candidates outside the
-// staged range read zero slots (idx is clamped to [0, hic]; both ends of the
-// buffer hold >= 4 zeros, and a clamp only happens for virtual slices j < 0 or
-// j >= nz, whose xa is 0).
+template <int NC>
+__device__ __forceinline__ float fw_row_sum(const float* xs, float rf, float A, float B, float E, float invB,
+                                            float cb, int off, int hic) {
+  const float cf = floorf(fmaf(rf, invB, cb));  // first candidate - 1
+  const int idx = min(max((int)cf + off, 0), hic);
+  float rlo, rhi;  // r - .5, r + .5 (exact); volatile so they are formed per active row, not per entry
+  asm volatile("{.reg .b64 ra, rd;\n\tmov.b64 ra, {%2, %2};\n\tadd.rn.f32x2 rd, ra, %3;\n\tmov.b64 {%0, %1}, rd;}"
+               : "=f"(rlo), "=f"(rhi) : "f"(rf), "l"(0x3f000000bf000000ull));
+  const float j0 = add_(cf, 1.0f);
+  const float2 T = fma2_(bc2_(B), make_float2(j0, add_(j0, 1.0f)), bc2_(A));
+  const float2 lo = add2_(T, bc2_(-E)), hi = add2_(T, bc2_(E));
+  float2 ov = add2_(make_float2(fminf(hi.x, rhi), fminf(hi.y, rhi)),
+                    make_float2(-fmaxf(lo.x, rlo), -fmaxf(lo.y, rlo)));
+  ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
+  const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
+  float p = add_(pp.x, pp.y);
+  if (NC == 3) {
+    const float T2 = fma_(B, add_(j0, 2.0f), A);
+    const float lo2 = add_(T2, -E), hi2 = add_(T2, E);
+    const float o2 = fmaxf(sub_(fminf(hi2, rhi), fmaxf(lo2, rlo)), 0.0f);
+    p = fma_(o2, xs[idx + 2], p);
+  }
+  return p;
+}
+
+// Rows of this lane in the 32-row groups [g0, g1], FW_RG groups per step (one
+// branch per block, so the independent row chains interleave; a row outside
+// [g0, g1] inside an active block adds exactly 0):
+// P(r) = sum over NC candidate slices j of tt(r, j) * xa(j), with T_j = A + B j
+// recomputed in registers (the same fma as the back kernel, so lo/hi are
+// bitwise equal) and only xa = amp * x staged in shared memory; then
+// y(r, c) += ts(c) P(r).  tt = max(0, min(hi, r+.5) - max(lo, r-.5)) equals
+// the back kernel's clamp(r+.5,lo,hi) - clamp(r-.5,lo,hi) bit for bit.
+// Candidates outside the staged range read zero slots (idx is clamped to
+// [0, hic]; both ends of the buffer hold >= 4 zeros, and a clamp only happens
+// for virtual slices j < 0 or j >= nz, whose xa is 0).
+#ifndef CTP_FW_RG
+#define CTP_FW_RG 3  // row groups evaluated per branch (independent chains that interleave)
+#endif
+constexpr int FW_RG = CTP_FW_RG;
+static_assert(FW_KR % FW_RG == 0, "row groups are processed in blocks of FW_RG");
+
 template <int NC>
 __device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
                                         const float* xs, float rbase, float A, float B, float E,
                                         float invB, float cb, int off, int hic, int g0, int g1) {
 #pragma unroll
-  for (int kk = 0; kk < FW_KR; ++kk) {
-    if (kk < g0 || kk > g1) continue;  // warp-uniform
-    const float rf = rbase + (float)(32 * kk);
-    const float cf = floorf(fmaf(rf, invB, cb));  // first candidate - 1
-    const int idx = min(max((int)cf + off, 0), hic);
-    const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
-    const float j0 = add_(cf, 1.0f);
-    const float2 T = fma2_(bc2_(B), make_float2(j0, add_(j0, 1.0f)), bc2_(A));
-    const float2 lo = add2_(T, bc2_(-E)), hi = add2_(T, bc2_(E));
-    float2 ov = add2_(make_float2(fminf(hi.x, rhi), fminf(hi.y, rhi)),
-                      make_float2(-fmaxf(lo.x, rlo), -fmaxf(lo.y, rlo)));
-    ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
-    const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
-    float p = add_(pp.x, pp.y);
-    if (NC == 3) {
-      const float T2 = fma_(B, add_(j0, 2.0f), A);
-      const float lo2 = add_(T2, -E), hi2 = add_(T2, E);
-      const float o2 = fmaxf(sub_(fminf(hi2, rhi), fmaxf(lo2, rlo)), 0.0f);
-      p = fma_(o2, xs[idx + 2], p);
-    }
-    const float2 p2 = bc2_(p);
+  for (int kk = 0; kk < FW_KR; kk += FW_RG) {
+    if (kk + FW_RG - 1 < g0 || kk > g1) continue;  // warp-uniform
+    float p[FW_RG];
+#pragma unroll
+    for (int q = 0; q < FW_RG; ++q)
+      p[q] = fw_row_sum<NC>(xs, rbase + (float)(32 * (kk + q)), A, B, E, invB, cb, off, hic);
 #pragma unroll
     for (int cc = 0; cc < FW_CW; cc += 2) {
-      const float2 a = fma2_(make_float2(ts[cc], ts[cc + 1]), p2, make_float2(acc[kk][cc], acc[kk][cc + 1]));
-      acc[kk][cc] = a.x;
-      acc[kk][cc + 1] = a.y;
+      const float2 t2 = make_float2(ts[cc], ts[cc + 1]);
+#pragma unroll
+      for (int q = 0; q < FW_RG; ++q) {
+        const float2 a = fma2_(t2, bc2_(p[q]), make_float2(acc[kk + q][cc], acc[kk + q][cc + 1]));
+        acc[kk + q][cc] = a.x;
+        acc[kk + q][cc + 1] = a.y;
+      }
     }
   }
 }
@@ -632,7 +656,8 @@ __device__ __forceinline__ void fw_prefetch(float4 (&xv)[FW_NLD], const float* _
   for (int t = 0; t < FW_NLD; ++t) {
     const int s = 4 * lane + 128 * t;
     if (VEC) {
-      xv[t] = s < nst ? __ldg(reinterpret_cast<const float4*>(xc + s)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      // slots >= nst are never staged: clamp to the last (valid) float4 instead of predicating
+      xv[t] = __ldg(reinterpret_cast<const float4*>(xc + min(s, (nst - 1) & ~3)));
     } else {
       xv[t].x = s < nst ? __ldg(xc + s) : 0.0f;
       xv[t].y = s + 1 < nst ? __ldg(xc + s + 1) : 0.0f;
@@ -653,8 +678,8 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
   float4 xv[FW_NLD];
   auto next_fast = [&](int e) {
     for (; e < nent; ++e) {
-      if (S.ent[e].info & (1 << 15)) {
-        fw_prefetch<VEC>(xv, xb + (size_t)S.ent[e].col * gp.nz + S.ent[e].za4, S.ent[e].nst, lane);
+      if (S.ent[e].info & (1 << 17)) {
+        fw_prefetch<VEC>(xv, xb + (unsigned)S.ent[e].col, S.ent[e].nst, lane);
         return e;
       }
     }
@@ -669,7 +694,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
     const float A = E.A, B = E.B, Eh = E.E, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
     const float invB = E.invB, cb = E.cb;
     const int za4 = E.za4;
-    const int g0 = info & 15, g1 = (info >> 4) & 15, nc = (info >> 8) & 127;
+    const int g0 = info & 31, g1 = (info >> 5) & 31, nc = (info >> 10) & 127;
     float ts[FW_CW];
 #pragma unroll
     for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
@@ -705,7 +730,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
     float P[FW_KR];
 #pragma unroll
     for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
-    const float* xc = xb + (size_t)E.col * gp.nz;
+    const float* xc = xb + (unsigned)(E.col - za4);
     for (int piece = za; piece <= zb; piece += FW_XCAP) {
       const int pe = min(piece + FW_XCAP - 1, zb);
       const int n = pe - piece + 1;
@@ -1153,6 +1178,7 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
   const size_t smem = forward_warp_smem_bytes();
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
+  if ((long long)gp.nx * gp.ny * gp.nz >= (1LL << 31)) return cudaErrorInvalidValue;  // 32-bit x offsets
   auto kern = vec ? sf_forward_kernel<true> : sf_forward_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
