@@ -83,10 +83,17 @@ __device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&
 // ---------------------------------------------------------------------------
 // back projection: x = A^T y
 // ---------------------------------------------------------------------------
-constexpr int BK_WARPS = 8;
-constexpr int BK_ZPL = 8;           // voxels per lane
+#ifndef CTP_BK_ZPL
+#define CTP_BK_ZPL 8
+#endif
+#ifndef CTP_BK_WARPS
+#define CTP_BK_WARPS 8
+#endif
+constexpr int BK_WARPS = CTP_BK_WARPS;  // warps per CTA (a 4 x BK_WARPS/4 block of voxel columns)
+constexpr int BK_ZPL = CTP_BK_ZPL;      // voxels per lane
+static_assert(BK_WARPS % 4 == 0, "CTAs cover 4 x BK_WARPS/4 voxel columns");
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
-constexpr int BK_QMAX = 480;        // per-warp row-sum table (rows): ZC * 1.8 + margin
+constexpr int BK_QMAX = BK_ZC * 15 / 8 + 0;  // per-warp row-sum table (rows): ZC * 1.8 + margin
 constexpr int BK_NCF = 4;           // footprint columns handled by the table path
 constexpr int BK_QUNROLL = CTP_BK_QUNROLL;  // row-sum loop unroll
 
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbx = (gp.nx + 3) >> 2;
   const int ix = (blockIdx.x % nbx) * 4 + (warp & 3);
-  const int iy = (blockIdx.x / nbx) * 2 + (warp >> 2);
+  const int iy = (blockIdx.x / nbx) * (BK_WARPS / 4) + (warp >> 2);
   if (ix >= gp.nx || iy >= gp.ny) return;  // warp-uniform; no CTA barriers below
   const int b = blockIdx.z;
   const int izs = blockIdx.y * BK_ZC;
@@ -436,6 +443,10 @@ constexpr int FW_CW = CTP_FW_CW;  // detector columns per tile
 #endif
 constexpr int FW_KR = CTP_FW_KR;     // 32-row groups per warp
 constexpr int FW_ROWS = 32 * FW_KR;  // rows per warp task
+#ifndef CTP_FW_VCH
+#define CTP_FW_VCH 16  // views per chunk of the task order (0: view-major within a band)
+#endif
+constexpr int FW_VCH = CTP_FW_VCH;
 static_assert(FW_KR <= 32, "row groups are 5-bit in FwEntry::info");
 constexpr int FW_XPAD = 4;           // zero slots below the staged slices
 // slices staged per entry (fast path) or per piece (generic path): the band's
@@ -510,7 +521,11 @@ __device__ __forceinline__ void band_info(FwEntry& e, const GridParams& gp, int 
   const bool empty = za > zb || r_lo > r_hi;
   e.za4 = za4;
   e.nst = empty ? 0 : zb - za4 + 1;
-  e.col = e.col * gp.nz + za4;  // 32-bit: the launcher checks nx*ny*nz < 2^31
+  // x offset of the first staged slice, 32-bit: in float4 units on the vector
+  // path (za4 and nz are multiples of 4), in floats otherwise; the launcher
+  // checks nx*ny*nz < 2^34 resp. 2^32
+  const unsigned xo = (unsigned)(((unsigned long long)(unsigned)e.col * (unsigned)gp.nz + (unsigned)za4) >> (vec ? 2 : 0));
+  e.col = (int)xo;
   const int g0 = (r_lo - rw0) >> 5, g1 = (r_hi - rw0) >> 5;
   const bool fast = !empty && e.nst <= FW_XCAP && nc <= 3;
   e.info = empty ? 0 : (g0 | (g1 << 5) | (min(nc, 127) << 10) | (fast ? (1 << 17) : 0));
@@ -679,7 +694,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
   auto next_fast = [&](int e) {
     for (; e < nent; ++e) {
       if (S.ent[e].info & (1 << 17)) {
-        fw_prefetch<VEC>(xv, xb + (unsigned)S.ent[e].col, S.ent[e].nst, lane);
+        fw_prefetch<VEC>(xv, xb + ((size_t)(unsigned)S.ent[e].col << (VEC ? 2 : 0)), S.ent[e].nst, lane);
         return e;
       }
     }
@@ -730,7 +745,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
     float P[FW_KR];
 #pragma unroll
     for (int kk = 0; kk < FW_KR; ++kk) P[kk] = 0.0f;
-    const float* xc = xb + (unsigned)(E.col - za4);
+    const float* xc = xb + (((size_t)(unsigned)E.col << (VEC ? 2 : 0)) - za4);
     for (int piece = za; piece <= zb; piece += FW_XCAP) {
       const int pe = min(piece + FW_XCAP - 1, zb);
       const int n = pe - piece + 1;
@@ -825,8 +840,20 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
   const long long per_band = (long long)ntiles * gp.nv * gp.batch;
   const int band = (int)(task / per_band);
   const long long t2 = task % per_band;
+#if CTP_FW_VCH > 0
+  // within a band: chunks of FW_VCH consecutive views, tiles, views of the
+  // chunk -- the CTAs resident at once cover a few dozen adjacent tiles over a
+  // few degrees of rotation, whose wedges (a fraction of the volume) stay in L2
+  const int nvb = gp.nv * gp.batch;
+  const int vch = (int)(t2 / ((long long)ntiles * FW_VCH));
+  const int rem = (int)(t2 - (long long)vch * ntiles * FW_VCH);
+  const int cv = min(FW_VCH, nvb - vch * FW_VCH);
+  const int tile = rem / cv;
+  const int vb = vch * FW_VCH + rem % cv;
+#else
   const int tile = (int)(t2 % ntiles);
   const int vb = (int)(t2 / ntiles);
+#endif
   const int v = vb % gp.nv, b = vb / gp.nv;
   const int c0 = tile * FW_CW;
   const int cw = min(FW_CW, gp.nc - c0);
@@ -1161,7 +1188,7 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
                         int batch, bool accumulate, cudaStream_t st) {
-  const int nbx = (gp.nx + 3) / 4, nby = (gp.ny + 1) / 2;
+  const int nbx = (gp.nx + 3) / 4, nby = (gp.ny + BK_WARPS / 4 - 1) / (BK_WARPS / 4);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = min(65535, batch - b0);
     const dim3 grid(nbx * nby, (gp.nz + BK_ZC - 1) / BK_ZC, nb);
@@ -1178,7 +1205,8 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
   const size_t smem = forward_warp_smem_bytes();
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
-  if ((long long)gp.nx * gp.ny * gp.nz >= (1LL << 31)) return cudaErrorInvalidValue;  // 32-bit x offsets
+  // 32-bit x offsets per entry (float4 units on the vector path)
+  if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
   auto kern = vec ? sf_forward_kernel<true> : sf_forward_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
