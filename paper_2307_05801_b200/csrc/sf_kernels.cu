@@ -321,14 +321,15 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     const int nsub = back_setup(gp, vcoef, vb, ix, iy, izs, ize, &my[lane][0]) ? 2 : 1;
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
-    for (int j = 0; j < nvb; ++j) {
+    const float* yview = yb + (size_t)vb * view_elems;  // [c][r] of view vb + j
+    for (int j = 0; j < nvb; ++j, yview += view_elems) {
 #pragma unroll 1
       for (int s = 0; s < nsub; ++s) {
         const BkEntry& ef = my[j][s];
         const int pk = ef.pk;
         if (pk & 1) {
           // fast path: everything precomputed; 4-row float4 row sums, then slices
-          const float* yv = yb + (size_t)(vb + j) * view_elems + ef.off0;
+          const float* yv = yview + ef.off0;
           const int n4 = (pk >> 4) & 0xfff;
           float4* q4 = reinterpret_cast<float4*>(qw);
           switch (ef.ncol) {  // warp-uniform: load only the footprint's columns
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
         const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
         const int Rz = first_row(sub_(fma_(e.B, (float)ize, e.A), e.E)) + K - 1;
         if (Rz < 0 || Ra > nr - 1) continue;
-        const float* yv = yb + (size_t)(vb + j) * view_elems;  // [c][r] of the view
+        const float* yv = yview;  // [c][r] of the view
         const int nq = Rz - Ra + 1;
         if (nq <= BK_QMAX && e.ncol <= BK_NCF && K <= 4) {
           // row sums Q(r) = sum_k ts_k y[cl+k][r]; absent columns have ts = 0 and
