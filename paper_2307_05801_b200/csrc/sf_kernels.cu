@@ -218,8 +218,24 @@ __device__ __forceinline__ float back_one_rows(float acc, const BkEntry& e, floa
 }
 
 template <int K>
+#ifndef CTP_BK_FULL
+#define CTP_BK_FULL 1  // straight-line slice pairs when every lane has BK_ZPL slices
+#endif
 __device__ __forceinline__ void back_slices(float (&acc)[BK_ZPL], const BkEntry& e, float izf0,
                                             int nvalid, const float* qw, int Ra) {
+#if CTP_BK_FULL
+  if (__all_sync(0xffffffffu, nvalid == BK_ZPL)) {  // the pair chains interleave
+#pragma unroll
+    for (int m = 0; m < BK_ZPL; m += 2) {
+      const float2 r = back_pair_rows<K>(make_float2(acc[m], acc[m + 1]), e,
+                                         make_float2(izf0 + (float)(32 * m), izf0 + (float)(32 * m + 32)),
+                                         qw, Ra);
+      acc[m] = r.x;
+      acc[m + 1] = r.y;
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int m = 0; m < BK_ZPL; m += 2) {
     if (m + 1 < nvalid) {
@@ -455,6 +471,11 @@ constexpr int FW_XPAD = 4;           // zero slots below the staged slices
 constexpr int FW_XCAP = ((32 * FW_KR + 64) + 127) / 128 * 128;
 constexpr int FW_XLEN = FW_XPAD + FW_XCAP + 4;  // + zero slots above
 constexpr int FW_NLD = FW_XCAP / 128;           // float4 x loads per lane (fast path)
+#ifndef CTP_FW_SG
+#define CTP_FW_SG 1  // staging loads per branch
+#endif
+constexpr int FW_SG = CTP_FW_SG;
+static_assert(FW_NLD % FW_SG == 0, "staging loads are processed in groups of FW_SG");
 
 struct FwEntry {
   int col;   // iy*nx + ix; band_info turns it into the x offset col*nz + za4 of the first staged slice
@@ -715,20 +736,24 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
 #pragma unroll
     for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
     if (e == e_pf) {
-      // stage xa = amp * x of slices za4 .. za4 + nst - 1 (4 per lane and load)
+      // stage xa = amp * x of slices za4 .. za4 + nst - 1 (4 per lane and load),
+      // FW_SG loads per branch so their chains interleave
 #pragma unroll
-      for (int t = 0; t < FW_NLD; ++t) {
-        const int s = 4 * lane + 128 * t;
-        if (128 * t >= nst) break;  // warp-uniform
-        const float z0 = (float)(za4 + s);
-        const float2 izA = make_float2(z0, add_(z0, 1.0f)), izB = make_float2(add_(z0, 2.0f), add_(z0, 3.0f));
-        const float2 qA = fma2_(bc2_(a1), izA, bc2_(a0)), qB = fma2_(bc2_(a1), izB, bc2_(a0));
-        const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
-        const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
-        const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
-        const float2 xaA = mul2_(ampA, make_float2(xv[t].x, xv[t].y));
-        const float2 xaB = mul2_(ampB, make_float2(xv[t].z, xv[t].w));
-        if (s < nst) *reinterpret_cast<float4*>(xs + FW_XPAD + s) = make_float4(xaA.x, xaA.y, xaB.x, xaB.y);
+      for (int t0 = 0; t0 < FW_NLD; t0 += FW_SG) {
+        if (128 * t0 >= nst) break;  // warp-uniform
+#pragma unroll
+        for (int t = t0; t < t0 + FW_SG; ++t) {
+          const int s = 4 * lane + 128 * t;
+          const float z0 = (float)(za4 + s);
+          const float2 izA = make_float2(z0, add_(z0, 1.0f)), izB = make_float2(add_(z0, 2.0f), add_(z0, 3.0f));
+          const float2 qA = fma2_(bc2_(a1), izA, bc2_(a0)), qB = fma2_(bc2_(a1), izB, bc2_(a0));
+          const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
+          const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
+          const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
+          const float2 xaA = mul2_(ampA, make_float2(xv[t].x, xv[t].y));
+          const float2 xaB = mul2_(ampB, make_float2(xv[t].z, xv[t].w));
+          if (s < nst) *reinterpret_cast<float4*>(xs + FW_XPAD + s) = make_float4(xaA.x, xaA.y, xaB.x, xaB.y);
+        }
       }
       if (lane < 4) xs[FW_XPAD + ((nst + 3) & ~3) + lane] = 0.0f;
       __syncwarp();
