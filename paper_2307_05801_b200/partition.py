@@ -1,4 +1,5 @@
-"""Single-box partitioner: views sharded across ranks (one process per GPU).
+"""Single-box partitioners (one process per GPU): views sharded across ranks
+(cone / modular), or z-slabs without any collective (parallel beam).
 
 north_star item (4).  The reference has no multi-device path (SURVEY.md
 section 0, gap 3); this module adds it around the unchanged single-GPU pair:
@@ -9,6 +10,10 @@ section 0, gap 3); this module adds it around the unchanged single-GPU pair:
   then ONE reduce-scatter (sum, fp32) over NCCL / NVLink leaves each rank the
   z-slab it owns of A^T y (``back``), or an all-reduce leaves every rank the
   whole volume (``back_replicated``).
+
+Parallel beam (``ZSlabParallelProjector``): rank r owns detector rows
+[r0, r1) in the forward and volume slices [z0, z1) in the back projection,
+with a one-slice / one-row halo; no communication.
 
 Because the sum over views is split into per-rank partial sums, the N-GPU
 back projection equals the 1-GPU result up to fp32 summation order;
@@ -152,3 +157,119 @@ def gather_slabs(slabs, nz: int):
     import torch
 
     return torch.cat(list(slabs), dim=1)[:, :nz]
+
+
+# --------------------------------------------------------------------------
+# parallel beam: z-slabs, no communication (north_star item 4)
+# --------------------------------------------------------------------------
+def even_ranges(n: int, world: int):
+    """Balanced contiguous [a, b) ranges of 0..n-1 over ``world`` ranks."""
+    if world > n:
+        raise ValueError(f"cannot split {n} items over {world} ranks")
+    return view_ranges(n, world)
+
+
+def _row_z(det, row_edge: float) -> float:
+    """World z of a detector row boundary (parallel beam: vax = +z, t = z)."""
+    return (row_edge - det.centerRow) * det.pixelHeight
+
+
+def rows_of_slices(g, spec, z0: int, z1: int):
+    """Detector rows [ra, rb) that slices [z0, z1) can reach (parallel beam:
+    rays have no z component, so slice iz only reaches the rows covering
+    [z_lo + iz hz, z_lo + (iz + 1) hz]; one row of margin each side)."""
+    det = g.detector
+    lo, _ = spec.bounds()
+    za, zb = lo[2] + z0 * spec.voxelHeight, lo[2] + z1 * spec.voxelHeight
+    ra = math.floor(za / det.pixelHeight + det.centerRow + 0.5) - 1
+    rb = math.ceil(zb / det.pixelHeight + det.centerRow - 0.5) + 2
+    return max(ra, 0), min(rb, det.numRows)
+
+
+def slices_of_rows(g, spec, r0: int, r1: int):
+    """Volume slices [za, zb) that rows [r0, r1) can receive from (one slice
+    of margin each side)."""
+    det = g.detector
+    lo, _ = spec.bounds()
+    za_w, zb_w = _row_z(det, r0 - 0.5), _row_z(det, r1 - 0.5)
+    za = math.floor((za_w - lo[2]) / spec.voxelHeight) - 1
+    zb = math.ceil((zb_w - lo[2]) / spec.voxelHeight) + 1
+    return max(za, 0), min(zb, spec.numZ)
+
+
+def row_subgeometry(g, r0: int, r1: int):
+    """The same scanner restricted to detector rows [r0, r1)."""
+    from dataclasses import replace
+
+    det = g.detector
+    return replace(g, detector=replace(det, numRows=r1 - r0, centerRow=det.centerRow - r0))
+
+
+class ZSlabParallelProjector:
+    """One rank's share of an N-way z-partitioned PARALLEL-beam SF pair.
+
+    Parallel rays have no z component (geometry.py pose table: vax = +z), so
+    detector row r only sees the slices covering its z range.  Forward: rank
+    r owns detector rows [r0, r1) of every view and projects the slices that
+    reach them (its row slab plus a one-slice halo); back: rank r owns volume
+    slices [z0, z1) and back-projects the rows that reach them (plus a
+    one-row halo).  Outputs are disjoint, inputs are read-only: no
+    collective at all.  Each sub-problem is a plan over a row sub-geometry
+    and a z-slab VolumeSpec, so only the fp32 rounding of the offsets
+    differs from the single-GPU pair (results equal within 1e-6).
+    """
+
+    def __init__(self, pair, rank: int, world: int, device=None, backend_factory=None):
+        from .chunking import slab_spec
+        from .geometry import PARALLEL
+        from .operator import ProjectorPair
+
+        g, spec = pair.geometry, pair.volumeSpec
+        if g.kind != PARALLEL:
+            raise ValueError("z-slab partitioning needs parallel-beam geometry (use ViewShardedProjector)")
+        self.full, self.rank, self.world = pair, rank, world
+        nr, nz = g.detector.numRows, spec.numZ
+        # forward: detector rows of this rank, the slices reaching them
+        self.rows = even_ranges(nr, world)[rank]
+        self.fwd_slices = slices_of_rows(g, spec, *self.rows)
+        a, b = self.fwd_slices
+        self.fwd_pair = (ProjectorPair(pair.model, row_subgeometry(g, *self.rows), slab_spec(spec, a, b - a))
+                         if b > a else None)
+        # back: volume slices of this rank, the rows reaching them
+        self.slices = even_ranges(nz, world)[rank]
+        self.back_rows = rows_of_slices(g, spec, *self.slices)
+        ra, rb = self.back_rows
+        z0, z1 = self.slices
+        self.back_pair = (ProjectorPair(pair.model, row_subgeometry(g, ra, rb), slab_spec(spec, z0, z1 - z0))
+                          if rb > ra else None)
+        if backend_factory is None:
+            idx = device.index if device is not None else 0
+            backend_factory = lambda p: CudaBackend(p, idx)  # noqa: E731
+        self._fwd = backend_factory(self.fwd_pair) if self.fwd_pair is not None else None
+        self._back = backend_factory(self.back_pair) if self.back_pair is not None else None
+
+    def forward(self, x):
+        """x [B, nz, ny, nx] (or just its slices ``fwd_slices``) -> rows
+        ``rows`` of every view [B, nv, r1 - r0, nc]."""
+        import torch
+
+        g = self.full.geometry
+        a, b = self.fwd_slices
+        if self._fwd is None:  # no slice reaches these rows
+            return torch.zeros((x.shape[0], g.numViews, self.rows[1] - self.rows[0], g.detector.numCols),
+                               dtype=torch.float32, device=x.device)
+        xs = x[:, a:b] if x.shape[1] == self.full.volumeSpec.numZ else x
+        return self._fwd.forward(xs.contiguous())
+
+    def back(self, y):
+        """y [B, nv, nr, nc] (or just its rows ``back_rows``) -> slices
+        ``slices`` of A^T y [B, z1 - z0, ny, nx]."""
+        import torch
+
+        spec = self.full.volumeSpec
+        ra, rb = self.back_rows
+        if self._back is None:  # these slices project outside the detector
+            return torch.zeros((y.shape[0], self.slices[1] - self.slices[0], spec.numY, spec.numX),
+                               dtype=torch.float32, device=y.device)
+        ys = y[:, :, ra:rb] if y.shape[2] == self.full.geometry.detector.numRows else y
+        return self._back.back(ys.contiguous())
