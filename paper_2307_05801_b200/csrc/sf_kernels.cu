@@ -188,7 +188,9 @@ __device__ __forceinline__ float2 back_pair_rows(float2 acc, const BkEntry& e, f
       gn = hi;
     } else {
       const float2 bnd = add2_(fl, bc2_((float)k + 1.5f));
-      gn = make_float2(clampf_(bnd.x, lo.x, hi.x), clampf_(bnd.y, lo.y, hi.y));
+      // bnd = fl + k + 1.5 > lo always (fl = floor(lo - .5) > lo - 1.5), so
+      // clamp(bnd, lo, hi) is exactly min(bnd, hi)
+      gn = make_float2(fminf(bnd.x, hi.x), fminf(bnd.y, hi.y));
     }
     const float2 c = mul2_(amp, add2_(gn, make_float2(-g.x, -g.y)));
     acc = fma2_(c, make_float2(qa[k], qb[k]), acc);
@@ -210,7 +212,7 @@ __device__ __forceinline__ float back_one_rows(float acc, const BkEntry& e, floa
   float g = lo;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const float gn = (k == K - 1) ? hi : clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+    const float gn = (k == K - 1) ? hi : fminf(add_(fl, (float)k + 1.5f), hi);  // (> lo, see above)
     acc = fma_(mul_(amp, add_(gn, -g)), qa[k], acc);
     g = gn;
   }
