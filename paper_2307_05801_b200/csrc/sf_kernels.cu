@@ -564,17 +564,30 @@ __device__ __forceinline__ float fw_row_sum(const float* xs, float rf, float A, 
   asm volatile("{.reg .b64 ra, rd;\n\tmov.b64 ra, {%2, %2};\n\tadd.rn.f32x2 rd, ra, %3;\n\tmov.b64 {%0, %1}, rd;}"
                : "=f"(rlo), "=f"(rhi) : "f"(rf), "l"(0x3f000000bf000000ull));
   const float j0 = add_(cf, 1.0f);
+  // The candidate window starts at most 0.99 slices past (r - .5 - E - A)/B
+  // and ends at least 0.01 past (r + .5 + E - A)/B (E = B/2), so the first
+  // candidate starts below the row (lo_0 < r - .5) and the last one ends above
+  // it (hi_last > r + .5), each by >= 0.01 B rows, far beyond fp32 rounding:
+  // max(lo_0, r - .5) is exactly r - .5 and min(hi_last, r + .5) exactly
+  // r + .5, and only the other bounds are evaluated.
   const float2 T = fma2_(bc2_(B), make_float2(j0, add_(j0, 1.0f)), bc2_(A));
-  const float2 lo = add2_(T, bc2_(-E)), hi = add2_(T, bc2_(E));
-  float2 ov = add2_(make_float2(fminf(hi.x, rhi), fminf(hi.y, rhi)),
-                    make_float2(-fmaxf(lo.x, rlo), -fmaxf(lo.y, rlo)));
-  ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
-  const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
-  float p = add_(pp.x, pp.y);
-  if (NC == 3) {
+  float p;
+  if (NC == 2) {
+    const float2 hl = add2_(T, make_float2(E, -E));  // (hi_0, lo_1)
+    float2 ov = add2_(make_float2(fminf(hl.x, rhi), rhi), make_float2(-rlo, -fmaxf(hl.y, rlo)));
+    ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
+    const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
+    p = add_(pp.x, pp.y);
+  } else {
+    const float2 hi = add2_(T, bc2_(E));  // (hi_0, hi_1)
+    const float lo1 = add_(T.y, -E);
+    float2 ov = add2_(make_float2(fminf(hi.x, rhi), fminf(hi.y, rhi)), make_float2(-rlo, -fmaxf(lo1, rlo)));
+    ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
+    const float2 pp = mul2_(ov, make_float2(xs[idx], xs[idx + 1]));
+    p = add_(pp.x, pp.y);
     const float T2 = fma_(B, add_(j0, 2.0f), A);
-    const float lo2 = add_(T2, -E), hi2 = add_(T2, E);
-    const float o2 = fmaxf(sub_(fminf(hi2, rhi), fmaxf(lo2, rlo)), 0.0f);
+    const float lo2 = add_(T2, -E);
+    const float o2 = fmaxf(sub_(rhi, fmaxf(lo2, rlo)), 0.0f);
     p = fma_(o2, xs[idx + 2], p);
   }
   return p;
