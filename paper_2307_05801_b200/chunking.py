@@ -34,7 +34,7 @@ import os
 from . import _native
 
 #: target bytes of sinogram per chunk (host<->device granularity)
-CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
+CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(1 << 30)))
 
 
 def _torch():
@@ -44,10 +44,15 @@ def _torch():
 
 
 def view_chunks(nv: int, view_bytes: int, chunk_bytes: int = CHUNK_BYTES):
-    """Contiguous [a, b) view ranges of about ``chunk_bytes`` each."""
+    """Contiguous [a, b) view ranges of about ``chunk_bytes`` each.  Chunks of
+    32 views or more are whole multiples of 32: the back kernel sets up 32
+    views per lane-parallel pass, so a ragged chunk would idle lanes."""
     per = max(1, min(nv, chunk_bytes // max(1, view_bytes)))
-    n = math.ceil(nv / per)
-    per = math.ceil(nv / n)
+    if per >= 32 and per < nv:
+        per = per // 32 * 32
+    else:
+        n = math.ceil(nv / per)
+        per = math.ceil(nv / n)
     return [(a, min(nv, a + per)) for a in range(0, nv, per)]
 
 
