@@ -1017,57 +1017,105 @@ __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const V
   float acc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g] = 0.0f;
+  const size_t view_stride = (size_t)gp.nc * Bs;
   for (int vb = 0; vb < gp.nv; vb += 32) {
-    {
-      const int v = vb + lane;
-      BkEntry e0, e1;
-      e0.ncol = 0;
-      e1.ncol = 0;
-      if (v < gp.nv) {
-        const ViewCoef vc = vcoef[v];
-        SubFoot f0, f1;
-        const int mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if (mask & 1) fill_entry(e0, f0, gp, 0, 0);
-        if (mask & 2) fill_entry(e1, f1, gp, 0, 0);
+    const int nsub = back_setup(gp, vcoef, vb, ix, iy, 0, 0, &my[lane][0]) ? 2 : 1;
+    // lane-parallel: the view's axial weight of row 0 times the amplitude,
+    // c = amp * tt (the 3D kernels' (amp * tt) factor), kept in the entry's
+    // lxy slot; entries that miss row 0 are dropped
+    bool narrow = true;  // no footprint wider than BK_NCF columns in this batch
+    for (int s = 0; s < nsub; ++s) {
+      BkEntry& e = my[lane][s];
+      bool hit = false;
+      const float tt = e.ncol > 0 ? row0_weight(e.A, e.B, e.E, hit) : 0.0f;
+      const float amp = mul_(e.lxy, sqrt_approx(fma_(e.a0, e.a0, 1.0f)));
+      if (!hit) e.ncol = 0;
+      if (e.ncol <= BK_NCF) {
+        // narrow: c = amp * tt, and a column window cl..cl+3 inside the
+        // detector whose weights outside the footprint are 0 (each adds an
+        // exact 0); missing entries get c = 0
+        e.lxy = e.ncol > 0 ? mul_(amp, tt) : 0.0f;
+        const int cl = min(e.ncol > 0 ? e.cl : 0, max(gp.nc - BK_NCF, 0));
+        float t[BK_NCF];
+#pragma unroll
+        for (int k = 0; k < BK_NCF; ++k) {
+          const int kk = cl + k - e.cl;  // index of column cl + k in the footprint's weights
+          t[k] = 0.0f;
+#pragma unroll
+          for (int m = 0; m < BK_NCF; ++m)
+            if (kk == m && m < e.ncol) t[k] = e.ts[m];
+        }
+#pragma unroll
+        for (int k = 0; k < BK_NCF; ++k) e.ts[k] = t[k];
+        e.cl = cl;
+      } else {
+        narrow = false;
       }
-      my[lane][0] = e0;
-      my[lane][1] = e1;
     }
+    narrow = __all_sync(0xffffffffu, narrow) && gp.nc >= BK_NCF;
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
-    for (int j = 0; j < nvb; ++j) {
-#pragma unroll 1
-      for (int s = 0; s < 2; ++s) {
-        const BkEntry e = my[j][s];
-        if (e.ncol == 0) continue;
-        bool hit;
-        const float tt = row0_weight(e.A, e.B, e.E, hit);
-        if (!hit) continue;
-        const float amp = mul_(e.lxy, sqrt_approx(fma_(e.a0, e.a0, 1.0f)));
-        const float c = mul_(amp, tt);
-        const float* yv = yB + (size_t)(vb + j) * gp.nc * Bs + b0;
-        Trap wide{};
-        if (e.ncol > BK_NCF) {
-          SubFoot f0, f1;
-          column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
-          wide = make_trap(s == 0 ? f0 : f1);
-        }
+    const float* yview = yB + (size_t)vb * view_stride + b0;
+    if (narrow && nsub == 1) {
+      // every entry of the batch is a narrow window: branch-free, unrolled
+      // over views so loads of consecutive views overlap
+#pragma unroll 4
+      for (int j = 0; j < nvb; ++j) {
+        const BkEntry& e = my[j][0];
+        const float c = e.lxy;
+        const float* yc = yview + (size_t)j * view_stride + (size_t)e.cl * Bs;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int b = lane + 32 * g;
           if (b >= nb) break;
-          float q = 0.0f;
-          if (e.ncol <= BK_NCF) {
+          float q = mul_(e.ts[0], __ldg(yc + b));
 #pragma unroll
-            for (int k = 0; k < BK_NCF; ++k)
-              if (k < e.ncol) q = fma_(e.ts[k], __ldg(yv + (size_t)(e.cl + k) * Bs + b), q);
-          } else {
-            float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
-            for (int k = 0; k < e.ncol; ++k) {
-              const float cur = trap_cum(wide, add_((float)(e.cl + k), 0.5f));
-              q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + k) * Bs + b), q);
-              prev = cur;
-            }
+          for (int k = 1; k < BK_NCF; ++k) q = fma_(e.ts[k], __ldg(yc + (size_t)k * Bs + b), q);
+          acc[g] = fma_(c, q, acc[g]);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    for (int j = 0; j < nvb; ++j, yview += view_stride) {
+#pragma unroll 1
+      for (int s = 0; s < nsub; ++s) {
+        const BkEntry& e = my[j][s];
+        const int ncol = e.ncol;
+        if (ncol == 0) continue;
+        if (ncol <= BK_NCF) {
+          const float c = e.lxy;
+          const float* yc = yview + (size_t)e.cl * Bs;
+          float t4[BK_NCF];
+#pragma unroll
+          for (int k = 0; k < BK_NCF; ++k) t4[k] = e.ts[k];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int b = lane + 32 * g;
+            if (b >= nb) break;
+            float q = mul_(t4[0], __ldg(yc + b));
+#pragma unroll
+            for (int k = 1; k < BK_NCF; ++k) q = fma_(t4[k], __ldg(yc + (size_t)k * Bs + b), q);  // (window)
+            acc[g] = fma_(c, q, acc[g]);
+          }
+          continue;
+        }
+        // wide footprint (> BK_NCF columns): rebuild its breakpoints
+        bool hit;
+        const float tt = row0_weight(e.A, e.B, e.E, hit);
+        const float c = mul_(mul_(e.lxy, sqrt_approx(fma_(e.a0, e.a0, 1.0f))), tt);
+        SubFoot f0, f1;
+        column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
+        const Trap wide = make_trap(s == 0 ? f0 : f1);
+        for (int g = 0; g < G; ++g) {
+          const int b = lane + 32 * g;
+          if (b >= nb) break;
+          float q = 0.0f;
+          float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
+          for (int k = 0; k < ncol; ++k) {
+            const float cur = trap_cum(wide, add_((float)(e.cl + k), 0.5f));
+            q = fma_(sub_(cur, prev), __ldg(yview + (size_t)(e.cl + k) * Bs + b), q);
+            prev = cur;
           }
           acc[g] = fma_(c, q, acc[g]);
         }
