@@ -1130,9 +1130,56 @@ __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const V
   }
 }
 
+// Fan-beam variant of fw_candidates: the footprint of candidate k = cbase +
+// lane, its tile test, and the fan-specific per-entry factors (axial weight
+// of row 0 in a1, amplitude in lxy), compacted into ent[0..); entries that
+// miss row 0 are dropped.  Out of line for the same register reasons.
+__device__ __noinline__ int fan_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp, FwEntry* ent,
+                                           int k, int total, int ib, int excl, int jl, bool primary_x, int c0,
+                                           int cw, float band_lo, float band_hi) {
+  const int lane = threadIdx.x & 31;
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int ex = __shfl_sync(0xffffffffu, excl, o + step);
+    if (ex <= k) o += step;
+  }
+  const int jo = __shfl_sync(0xffffffffu, jl, o);
+  const int exo = __shfl_sync(0xffffffffu, excl, o);
+  SubFoot f[2];
+  float tt[2] = {0.0f, 0.0f};
+  int mask = 0, col = 0;
+  if (k < total) {
+    const ViewCoef vc = *vcp;
+    const int ii = ib + o, j = jo + (k - exo);
+    const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
+    col = iy * gp.nx + ix;
+    mask = column_footprint(vc, gp, ix, iy, f[0], f[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!(mask & (1 << h))) continue;
+      bool hit = false;
+      if (reaches_tile(f[h], gp, c0, cw, band_lo, band_hi)) tt[h] = row0_weight(f[h].A, f[h].B, f[h].E, hit);
+      if (!hit) mask &= ~(1 << h);
+    }
+  }
+  const int n = __popc(mask);
+  const int ni = warp_incl_scan(n, lane);
+  int off = ni - n;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(mask & (1 << h))) continue;
+    FwEntry& e = ent[off++];
+    write_entry(e, f[h], col, c0, cw);
+    e.a1 = tt[h];
+    e.lxy = mul_(f[h].lxy, sqrt_approx(fma_(f[h].a0, f[h].a0, 1.0f)));  // amp at iz = 0
+  }
+  return __shfl_sync(0xffffffffu, ni, 31);
+}
+
 template <int G>
 __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
-    GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xB,  // [ny*nx][Bs]
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xB,  // [ny*nx][Bs]
     float* __restrict__ yB,                                                         // [nv][nc][Bs]
     int Bs, int b0, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1168,12 +1215,10 @@ __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
 
   int pending = 0;
   auto flush = [&]() {
+#pragma unroll 2
     for (int e = 0; e < pending; ++e) {
       const FwEntry& E = ent[e];
-      bool hit;
-      const float tt = row0_weight(E.A, E.B, E.E, hit);
-      if (!hit) continue;
-      const float amp = mul_(E.lxy, sqrt_approx(fma_(E.a0, E.a0, 1.0f)));
+      const float tt = E.a1, amp = E.lxy;  // set up by fan_candidates
       const float* xc = xB + (size_t)E.col * Bs + b0;
       float ts[FW_CW];
 #pragma unroll
@@ -1217,31 +1262,8 @@ __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
     const int excl = incl - cnt;
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
-      const int k = cbase + lane;
-      int o = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int ex = __shfl_sync(0xffffffffu, excl, o + step);
-        if (ex <= k) o += step;
-      }
-      const int jo = __shfl_sync(0xffffffffu, jl, o);
-      const int exo = __shfl_sync(0xffffffffu, excl, o);
-      SubFoot f0, f1;
-      int mask = 0, col = 0;
-      if (k < total) {
-        const int ii = ib + o, j = jo + (k - exo);
-        const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
-        col = iy * gp.nx + ix;
-        mask = column_footprint(vc, gp, ix, iy, f0, f1);
-        if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
-        if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
-      }
-      const int n = __popc(mask);
-      const int ni = warp_incl_scan(n, lane);
-      const int off = pending + ni - n;
-      if (mask & 1) write_entry(ent[off], f0, col, c0, cw);
-      if (mask & 2) write_entry(ent[off + (mask & 1)], f1, col, c0, cw);
-      pending += __shfl_sync(0xffffffffu, ni, 31);
+      pending += fan_candidates(gp, vcoef + v, ent + pending, cbase + lane, total, ib, excl, jl, primary_x, c0,
+                                cw, band_lo, band_hi);
       __syncwarp();
       if (pending >= 32) {
         flush();
