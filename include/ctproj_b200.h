@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define CTP_ABI_VERSION 1
+#define CTP_ABI_VERSION 2
 
 /* geometry kinds; same codes as KIND_CODE (pkg/src/ctproj/_common.py:5) */
 enum ctp_kind {
@@ -132,6 +132,23 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch,
  * in `direction` (0 forward, 1 back) on this plan.  Synchronises on the
  * recorded end event.  Returns CTP_ERR_INVALID_ARGUMENT if none was recorded. */
 int ctp_plan_kernel_time_ms(const ctp_plan* plan, int direction, float* ms);
+
+/* Siddon pair (exact ray-voxel line lengths, float64 like the reference):
+ *   ctp_siddon_forward <- siddon_forward_kernel(vol, out, kind, src, c0, u, vax,
+ *                         w, pw, ph, cr, cc, sdd, back, x0, y0, z0, hx, hz)
+ *                         (pkg/src/ctproj/_kernels.py:191-208), called by
+ *                         siddon_forward (pkg/src/ctproj/siddon.py:18-23);
+ *   ctp_siddon_back    <- siddon_back_kernel(y, out, ...same...)
+ *                         (_kernels.py:282-387), called by siddon_backproject
+ *                         (siddon.py:26-31).
+ * `back` is kernel_geom's parallel-beam ray back-off (circumscribed radius of
+ * the grid plus one voxel width, _common.py:21-24); it only matters for
+ * parallel geometry.  No workspace; same layouts, flags and contract as the
+ * SF entry points.  Every geometry kind, modular included, is supported. */
+int ctp_siddon_forward(const ctp_plan* plan, double back, const float* vol, float* sino,
+                       int batch, uint32_t flags, void* stream);
+int ctp_siddon_back(const ctp_plan* plan, double back, const float* sino, float* vol,
+                    int batch, uint32_t flags, void* stream);
 
 /* One-shot variants with the reference kernel's shape: they build a
  * temporary plan, allocate workspace stream-ordered, launch, and release.

@@ -41,13 +41,16 @@ def plan_for(g: Geometry, spec: VolumeSpec, device_index: int | None = None) -> 
     return _native.get_plan(g, spec, device_index)
 
 
-def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None):
-    """Apply A / A^T to ``batch`` ([B, *in_shape]); returns [B, *out_shape]."""
+def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None, model: str = "sf"):
+    """Apply A / A^T of ``model`` ("sf" or "siddon") to ``batch``
+    ([B, *in_shape]); returns [B, *out_shape]."""
     torch = _torch()
     in_shape = spec.shape if direction == 0 else g.shape
     if tuple(batch.shape[1:]) != tuple(in_shape):
         raise SpecMismatchError(f"batch must have shape (B, {', '.join(map(str, in_shape))}), "
                                 f"got {tuple(batch.shape)}")
+    if model == "siddon":
+        return _run_siddon(g, spec, batch, direction, out)
     if isinstance(batch, torch.Tensor) and batch.is_cuda:
         plan = plan_for(g, spec, batch.device.index)
         x = batch if batch.dtype == torch.float32 else batch.to(torch.float32)
@@ -66,6 +69,28 @@ def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None):
         res = zslab_apply(plan, host, direction, nzs)
     else:
         res = host_apply(plan, host, direction)
+    return res.numpy() if as_numpy else res
+
+
+def _run_siddon(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None):
+    """Siddon pair: CUDA tensors stay on the device; host arrays / CPU tensors
+    go up through pinned memory, are projected in one launch, and come back
+    as the same kind (no view chunking: this model is not the hot path)."""
+    torch = _torch()
+    if isinstance(batch, torch.Tensor) and batch.is_cuda:
+        plan = plan_for(g, spec, batch.device.index)
+        x = batch if batch.dtype == torch.float32 else batch.to(torch.float32)
+        x = x.contiguous()
+        with torch.cuda.device(batch.device):
+            return plan.siddon_forward(x, out=out) if direction == 0 else plan.siddon_back(x, out=out)
+    plan = plan_for(g, spec)
+    as_numpy = not isinstance(batch, torch.Tensor)
+    host = torch.from_numpy(np.ascontiguousarray(batch, dtype=np.float32)) if as_numpy else batch
+    host = host.to(torch.float32).contiguous()
+    with torch.cuda.device(plan.device):
+        xd = host.pin_memory().to(plan.device, non_blocking=True)
+        res = plan.siddon_forward(xd) if direction == 0 else plan.siddon_back(xd)
+        res = res.cpu()
     return res.numpy() if as_numpy else res
 
 

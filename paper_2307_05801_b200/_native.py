@@ -30,7 +30,7 @@ from .geometry import Geometry, VolumeSpec, kernel_args
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CTPROJ_LIB") or os.path.join(_HERE, "csrc", "libctproj_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 CTP_OK = 0
 _STATUS_ERRORS = {
@@ -58,6 +58,8 @@ EXPORTED_SYMBOLS = (
     "ctp_plan_kernel_time_ms",
     "ctp_sf_forward_oneshot",
     "ctp_sf_back_oneshot",
+    "ctp_siddon_forward",
+    "ctp_siddon_back",
 )
 
 
@@ -131,6 +133,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         for name in ("ctp_sf_forward_oneshot", "ctp_sf_back_oneshot"):
             fn = getattr(lib, name)
             fn.argtypes = [ctypes.POINTER(CtpGeom), vp, vp, i32, vp]
+            fn.restype = i32
+        for name in ("ctp_siddon_forward", "ctp_siddon_back"):
+            fn = getattr(lib, name)
+            fn.argtypes = [vp, ctypes.c_double, vp, vp, i32, u32, vp]
             fn.restype = i32
         if lib.ctp_abi_version() != ABI_VERSION:
             raise NativeLibraryError(
@@ -207,6 +213,35 @@ class Plan:
         if st != CTP_OK:
             _raise_status(self.lib, st, "ctp_sf_forward" if direction == 0 else "ctp_sf_back")
         return out
+
+    def _run_siddon(self, direction: int, inp, out, accumulate: bool, time_kernel: bool = False):
+        import torch
+
+        # kernel_geom's parallel-beam ray back-off (_common.py:21-24), same expression
+        back = float(self.spec.circumscribed_radius() + self.spec.voxelWidth)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        fn = self.lib.ctp_siddon_forward if direction == 0 else self.lib.ctp_siddon_back
+        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_TIME_KERNEL if time_kernel else 0)
+        st = fn(self._h, back, inp.data_ptr(), out.data_ptr(), int(inp.shape[0]), flags, stream)
+        if st != CTP_OK:
+            _raise_status(self.lib, st, "ctp_siddon_forward" if direction == 0 else "ctp_siddon_back")
+        return out
+
+    def siddon_forward(self, x, out=None, accumulate: bool = False, time_kernel: bool = False):
+        """Siddon y = A x on device tensors (same layouts as ``forward``)."""
+        import torch
+
+        if out is None:
+            out = torch.empty((x.shape[0],) + self.sino_shape, dtype=torch.float32, device=self.device)
+        return self._run_siddon(0, x, out, accumulate, time_kernel)
+
+    def siddon_back(self, y, out=None, accumulate: bool = False, time_kernel: bool = False):
+        """Siddon x = A^T y on device tensors (same layouts as ``back``)."""
+        import torch
+
+        if out is None:
+            out = torch.empty((y.shape[0],) + self.vol_shape, dtype=torch.float32, device=self.device)
+        return self._run_siddon(1, y, out, accumulate, time_kernel)
 
     def forward(self, x, out=None, accumulate: bool = False, time_kernel: bool = False):
         """y[B, nv, nr, nc] = A x[B, nz, ny, nx]; device tensors, f32, contiguous."""

@@ -26,6 +26,9 @@ struct ctp_plan {
   std::vector<double> poses;   // host copy, nv*15
   int device;
   ViewCoef* d_coef;            // device, nv entries
+  double* d_pose;              // device, nv*15 float64 (Siddon pair)
+  bool sf_ok;                  // SF supports this geometry (SF-modular needs rowDir.z > 0.05)
+  std::string sf_reason;
   GridParams gp;
   size_t vol_elems, sino_elems;
   cudaEvent_t ev[2][2];        // [direction][start/stop], created lazily
@@ -85,14 +88,16 @@ int validate(const ctp_geom* g) {
     return fail(CTP_ERR_INVALID_ARGUMENT, "array too large");
   for (long long k = 0; k < 15LL * g->num_views; ++k)
     if (!std::isfinite(g->poses[k])) return fail(CTP_ERR_INVALID_ARGUMENT, "non-finite pose entry");
-  if (g->kind == CTP_MODULAR) {
-    // the SF-modular model keeps detector rows increasing with z
-    for (int v = 0; v < g->num_views; ++v)
-      if (!(g->poses[15 * v + 11] > 0.05))
-        return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
-                    "SF-modular needs rowDir with a positive z component (> 0.05) in every view");
-  }
   return CTP_OK;
+}
+
+// the SF-modular model keeps detector rows increasing with z (the Siddon pair
+// has no such restriction, so this is checked per model, not per plan)
+bool sf_supports(const ctp_geom* g) {
+  if (g->kind != CTP_MODULAR) return true;
+  for (int v = 0; v < g->num_views; ++v)
+    if (!(g->poses[15 * v + 11] > 0.05)) return false;
+  return true;
 }
 
 // float64 digestion of one view's pose into affine footprint coefficients
@@ -310,11 +315,16 @@ int ctp_plan_create(const ctp_geom* geom, int device, ctp_plan** plan_out) {
     return cuda_fail(e, "cudaMalloc(view coefficients)");
   }
   e = cudaMemcpy(p->d_coef, coefs.data(), sizeof(ViewCoef) * coefs.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_pose, sizeof(double) * p->poses.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_pose, p->poses.data(), sizeof(double) * p->poses.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(p->d_coef);
+    if (p->d_pose) cudaFree(p->d_pose);
     delete p;
-    return cuda_fail(e, "upload view coefficients");
+    return cuda_fail(e, "upload view tables");
   }
+  p->sf_ok = sf_supports(geom);
   *plan_out = p;
   return CTP_OK;
 }
@@ -323,6 +333,7 @@ int ctp_plan_destroy(ctp_plan* plan) {
   if (!plan) return CTP_OK;
   DeviceGuard guard(plan->device);
   if (plan->d_coef) cudaFree(plan->d_coef);
+  if (plan->d_pose) cudaFree(plan->d_pose);
   for (int d = 0; d < 2; ++d)
     for (int k = 0; k < 2; ++k)
       if (plan->ev[d][k]) cudaEventDestroy(plan->ev[d][k]);
@@ -350,10 +361,18 @@ size_t ctp_sf_workspace_bytes(const ctp_plan* plan, int direction, int batch) {
   return align_up(per * sizeof(float) * (size_t)batch);
 }
 
+static int check_sf(const ctp_plan* plan) {
+  if (plan && !plan->sf_ok)
+    return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
+                "SF-modular needs rowDir with a positive z component (> 0.05) in every view");
+  return CTP_OK;
+}
+
 int ctp_sf_forward(const ctp_plan* plan, const float* vol, float* sino, int batch, void* workspace,
                    size_t workspace_bytes, uint32_t flags, void* stream) {
   const size_t need = plan ? ctp_sf_workspace_bytes(plan, 0, batch) : 0;
   int st = check_run_args(plan, vol, sino, batch, workspace, workspace_bytes, need);
+  if (st == CTP_OK) st = check_sf(plan);
   if (st != CTP_OK) return st;
   DeviceGuard guard(plan->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
@@ -386,6 +405,7 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
                 size_t workspace_bytes, uint32_t flags, void* stream) {
   const size_t need = plan ? ctp_sf_workspace_bytes(plan, 1, batch) : 0;
   int st = check_run_args(plan, sino, vol, batch, workspace, workspace_bytes, need);
+  if (st == CTP_OK) st = check_sf(plan);
   if (st != CTP_OK) return st;
   DeviceGuard guard(plan->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
@@ -411,6 +431,61 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
   e = ctp::launch_back(gp, plan->d_coef, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
   timer.stop();
   if (e != cudaSuccess) return cuda_fail(e, "sf_back_kernel");
+  return CTP_OK;
+}
+
+static ctp::SiddonParams siddon_params(const ctp_geom& g, double back) {
+  ctp::SiddonParams p;
+  p.kind = g.kind;
+  p.nv = g.num_views;
+  p.nr = g.num_rows;
+  p.nc = g.num_cols;
+  p.nx = g.num_x;
+  p.ny = g.num_y;
+  p.nz = g.num_z;
+  p.pw = g.pixel_width;
+  p.ph = g.pixel_height;
+  p.cr = g.center_row;
+  p.cc = g.center_col;
+  p.sdd = g.sdd;
+  p.back = back;
+  p.x0 = g.x0;
+  p.y0 = g.y0;
+  p.z0 = g.z0;
+  p.hx = g.voxel_width;
+  p.hz = g.voxel_height;
+  return p;
+}
+
+int ctp_siddon_forward(const ctp_plan* plan, double back, const float* vol, float* sino, int batch,
+                       uint32_t flags, void* stream) {
+  int st = check_run_args(plan, vol, sino, batch, nullptr, 0, 0);
+  if (st != CTP_OK) return st;
+  if (!std::isfinite(back)) return fail(CTP_ERR_INVALID_ARGUMENT, "back must be finite");
+  DeviceGuard guard(plan->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  KernelTimer timer(plan, 0, s, flags);
+  cudaError_t e = ctp::launch_siddon_forward(siddon_params(plan->geom, back), plan->d_pose, vol, sino, batch,
+                                             (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  timer.stop();
+  if (e != cudaSuccess) return cuda_fail(e, "siddon_forward_kernel");
+  return CTP_OK;
+}
+
+int ctp_siddon_back(const ctp_plan* plan, double back, const float* sino, float* vol, int batch,
+                    uint32_t flags, void* stream) {
+  int st = check_run_args(plan, sino, vol, batch, nullptr, 0, 0);
+  if (st != CTP_OK) return st;
+  if (!std::isfinite(back)) return fail(CTP_ERR_INVALID_ARGUMENT, "back must be finite");
+  DeviceGuard guard(plan->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  KernelTimer timer(plan, 1, s, flags);
+  cudaError_t e = ctp::launch_siddon_back(siddon_params(plan->geom, back), plan->d_pose, sino, vol, batch,
+                                          (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  timer.stop();
+  if (e != cudaSuccess) return cuda_fail(e, "siddon_back_kernel");
   return CTP_OK;
 }
 

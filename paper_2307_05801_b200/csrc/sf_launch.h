@@ -1,5 +1,5 @@
 // sf_launch.h -- internal launcher interface between the C-ABI (capi.cu) and
-// the kernels (sf_kernels.cu).  Not part of the public ABI.
+// the kernels (sf_kernels.cu, siddon_kernels.cu).  Not part of the public ABI.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,5 +24,17 @@ cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, cons
                                int batch, cudaStream_t st);
 cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
                             int batch, cudaStream_t st);
+
+// Siddon pair (siddon_kernels.cu): the float64 scalars of kernel_geom
+// (_common.py:8-39) including the parallel-beam ray back-off `back`
+struct SiddonParams {
+  int kind, nv, nr, nc, nx, ny, nz;
+  double pw, ph, cr, cc, sdd, back, x0, y0, z0, hx, hz;
+};
+// poses: device [nv][15] float64 (src, c0, u, vax, w); natural layouts
+cudaError_t launch_siddon_forward(const SiddonParams& p, const double* poses, const float* vol, float* sino,
+                                  int batch, bool accumulate, cudaStream_t st);
+cudaError_t launch_siddon_back(const SiddonParams& p, const double* poses, const float* sino, float* vol,
+                               int batch, bool accumulate, cudaStream_t st);
 
 }  // namespace ctp

@@ -56,10 +56,12 @@ class CudaBackend:
     device_index: int
 
     def forward(self, x, out=None):
-        return self.pair.plan(self.device_index).forward(x, out=out)
+        plan = self.pair.plan(self.device_index)
+        return (plan.siddon_forward if self.pair.model == "siddon" else plan.forward)(x, out=out)
 
     def back(self, y, out=None):
-        return self.pair.plan(self.device_index).back(y, out=out)
+        plan = self.pair.plan(self.device_index)
+        return (plan.siddon_back if self.pair.model == "siddon" else plan.back)(y, out=out)
 
 
 class ViewShardedProjector:

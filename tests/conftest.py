@@ -13,14 +13,15 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "sf_golden.npz")
+SIDDON_GOLDEN = os.path.join(ROOT, "tests", "golden", "siddon_golden.npz")
 
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
 
 
-def load_golden():
-    z = np.load(GOLDEN)
+def load_golden(path=GOLDEN):
+    z = np.load(path)
     cases = {}
     for key in z.files:
         name, field = key.split(".", 1)
@@ -38,6 +39,11 @@ def load_golden():
 @pytest.fixture(scope="session")
 def golden():
     return load_golden()
+
+
+@pytest.fixture(scope="session")
+def siddon_golden():
+    return load_golden(SIDDON_GOLDEN)
 
 
 @pytest.fixture(scope="session")

@@ -133,7 +133,7 @@ def test_binding_autograd_is_native_adjoint_bitwise(golden, tmp_path):
     c = golden["parallel_small"]
     cfg = tmp_path / "cfg.json"
     cfg.write_text(json.dumps(c["config"]))
-    proj = load_param(cfg)
+    proj = load_param(cfg, model=ct.SF)
     P = proj.pair
     x = torch.rand((1,) + P.volumeSpec.shape, device=DEV, requires_grad=True)
     ybar = torch.rand((1,) + P.geometry.shape, device=DEV)

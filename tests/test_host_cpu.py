@@ -113,8 +113,9 @@ def test_pair_model_checks():
     with pytest.raises(errors.UnsupportedGeometryError):
         ct.ProjectorPair(ct.SF, ct.Geometry(kind=ct.MODULAR, detector=g.detector,
                                             modularViews=flipped), spec)
-    with pytest.raises(errors.UnsupportedGeometryError):
-        ct.ProjectorPair(ct.SIDDON, g, spec)
+    # the Siddon pair exists for every kind, modular poses of any orientation included
+    ct.ProjectorPair(ct.SIDDON, g, spec)
+    ct.ProjectorPair(ct.SIDDON, ct.Geometry(kind=ct.MODULAR, detector=g.detector, modularViews=flipped), spec)
 
 
 def test_apply_spec_mismatch():
