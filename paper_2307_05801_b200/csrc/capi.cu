@@ -481,10 +481,20 @@ int ctp_siddon_back(const ctp_plan* plan, double back, const float* sino, float*
   DeviceGuard guard(plan->device);
   if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const ctp::SiddonParams sp = siddon_params(plan->geom, back);
+  // stream-ordered scratch for the per-pixel ray table (skipped above 8 GiB:
+  // the gather then recomputes each ray)
+  const size_t tb = ctp::siddon_ray_table_bytes(sp);
+  void* table = nullptr;
+  if (tb <= (size_t(8) << 30) && cudaMallocAsync(&table, tb, s) != cudaSuccess) {
+    cudaGetLastError();  // clear; fall back to recomputing the rays
+    table = nullptr;
+  }
   KernelTimer timer(plan, 1, s, flags);
-  cudaError_t e = ctp::launch_siddon_back(siddon_params(plan->geom, back), plan->d_pose, sino, vol, batch,
-                                          (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  cudaError_t e = ctp::launch_siddon_back(sp, plan->d_pose, sino, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0,
+                                          table, s);
   timer.stop();
+  if (table) cudaFreeAsync(table, s);
   if (e != cudaSuccess) return cuda_fail(e, "siddon_back_kernel");
   return CTP_OK;
 }

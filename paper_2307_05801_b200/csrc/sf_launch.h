@@ -34,7 +34,10 @@ struct SiddonParams {
 // poses: device [nv][15] float64 (src, c0, u, vax, w); natural layouts
 cudaError_t launch_siddon_forward(const SiddonParams& p, const double* poses, const float* vol, float* sino,
                                   int batch, bool accumulate, cudaStream_t st);
+// ray_table: device scratch of siddon_ray_table_bytes(p) bytes, or nullptr to
+// recompute the rays in the gather
+size_t siddon_ray_table_bytes(const SiddonParams& p);
 cudaError_t launch_siddon_back(const SiddonParams& p, const double* poses, const float* sino, float* vol,
-                               int batch, bool accumulate, cudaStream_t st);
+                               int batch, bool accumulate, void* ray_table, cudaStream_t st);
 
 }  // namespace ctp

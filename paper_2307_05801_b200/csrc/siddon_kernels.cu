@@ -235,7 +235,24 @@ __global__ void __launch_bounds__(256) siddon_forward_kernel(SiddonParams p, con
   *o = accumulate ? *o + val : val;
 }
 
+// ray table for the back projector: rays[(view*nr + row)*nc + col] = the
+// same Ray sample_ray returns (bitwise), so the gather need not recompute the
+// normalisation (sqrt + 3 divisions) for each of its ~20 candidate pixels
+__global__ void __launch_bounds__(256) siddon_rays_kernel(SiddonParams p, const double* __restrict__ poses,
+                                                          Ray* __restrict__ rays) {
+  const long long nray = (long long)p.nv * p.nr * p.nc;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nray) return;
+  const int view = (int)(idx / ((long long)p.nr * p.nc));
+  const long long rem = idx - (long long)view * p.nr * p.nc;
+  const int row = (int)(rem / p.nc);
+  const int col = (int)(rem - (long long)row * p.nc);
+  rays[idx] = sample_ray(p, poses + 15 * view, row, col);
+}
+
+template <bool TABLE>
 __global__ void __launch_bounds__(256) siddon_back_kernel(SiddonParams p, const double* __restrict__ poses,
+                                                          const Ray* __restrict__ rays,
                                                           const float* __restrict__ sino,
                                                           float* __restrict__ vol, int accumulate) {
   const long long nvox = (long long)p.nx * p.ny * p.nz;
@@ -248,6 +265,8 @@ __global__ void __launch_bounds__(256) siddon_back_kernel(SiddonParams p, const 
   const int ix = (int)(rem - (long long)iy * p.nx);
   const double xlo = p.x0 + ix * p.hx, ylo = p.y0 + iy * p.hx, zlo = p.z0 + iz * p.hz;
   const double xhi = xlo + p.hx, yhi = ylo + p.hx, zhi = zlo + p.hz;
+  const double cx = xlo + 0.5 * p.hx, cy = ylo + 0.5 * p.hx, cz = zlo + 0.5 * p.hz;
+  const double rad2 = (0.5 * p.hx * p.hx + 0.25 * p.hz * p.hz) * (1.0 + 1e-6) + 1e-12;  // (half-diagonal)^2
   const float* yb = sino + (size_t)b * p.nv * p.nr * p.nc;
   double acc = 0.0;
   for (int view = 0; view < p.nv; ++view) {
@@ -277,9 +296,18 @@ __global__ void __launch_bounds__(256) siddon_back_kernel(SiddonParams p, const 
       r1 = min((int)floor(tmax / p.ph + p.cr + 0.5) + 1, p.nr - 1);
     }
     const float* yv = yb + (size_t)view * p.nr * p.nc;
+    const Ray* rv = rays + (size_t)view * p.nr * p.nc;
     for (int row = r0; row <= r1; ++row) {
       for (int col = cl; col <= ch; ++col) {
-        const Ray r = sample_ray(p, P, row, col);
+        const Ray r = TABLE ? rv[(size_t)row * p.nc + col] : sample_ray(p, P, row, col);
+        // a ray that meets the box passes within its half-diagonal of the
+        // centre; rays clearly farther (the window's padding) contribute an
+        // exact 0 and skip the clip (unit directions; the margin dwarfs the
+        // rounding of dist2)
+        const double vx = cx - r.ox, vy = cy - r.oy, vz = cz - r.oz;
+        const double pr = vx * r.dx + vy * r.dy + vz * r.dz;
+        const double dist2 = vx * vx + vy * vy + vz * vz - pr * pr;
+        if (dist2 > rad2) continue;
         const double ln = ray_box_len(r, xlo, xhi, ylo, yhi, zlo, zhi);
         if (ln > 0.0) acc += ln * (double)__ldg(yv + (size_t)row * p.nc + col);
       }
@@ -304,14 +332,27 @@ cudaError_t launch_siddon_forward(const SiddonParams& p, const double* poses, co
   return cudaGetLastError();
 }
 
+size_t siddon_ray_table_bytes(const SiddonParams& p) {
+  return sizeof(Ray) * (size_t)p.nv * p.nr * p.nc;
+}
+
 cudaError_t launch_siddon_back(const SiddonParams& p, const double* poses, const float* sino, float* vol,
-                               int batch, bool accumulate, cudaStream_t st) {
+                               int batch, bool accumulate, void* ray_table, cudaStream_t st) {
   const long long nvox = (long long)p.nx * p.ny * p.nz;
+  Ray* rays = static_cast<Ray*>(ray_table);
+  if (rays) {
+    const long long nray = (long long)p.nv * p.nr * p.nc;
+    siddon_rays_kernel<<<(unsigned)((nray + 255) / 256), 256, 0, st>>>(p, poses, rays);
+  }
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = batch - b0 < 65535 ? batch - b0 : 65535;
     const dim3 grid((unsigned)((nvox + 255) / 256), nb);
-    siddon_back_kernel<<<grid, 256, 0, st>>>(p, poses, sino + (size_t)b0 * p.nv * p.nr * p.nc,
-                                             vol + (size_t)b0 * nvox, accumulate ? 1 : 0);
+    const float* sb = sino + (size_t)b0 * p.nv * p.nr * p.nc;
+    float* vb = vol + (size_t)b0 * nvox;
+    if (rays)
+      siddon_back_kernel<true><<<grid, 256, 0, st>>>(p, poses, rays, sb, vb, accumulate ? 1 : 0);
+    else
+      siddon_back_kernel<false><<<grid, 256, 0, st>>>(p, poses, nullptr, sb, vb, accumulate ? 1 : 0);
   }
   return cudaGetLastError();
 }
