@@ -60,3 +60,17 @@ def test_oracle_rejects_modular(oracle_mod):
     cfg = {"geometry": "modular", "views": []}
     with pytest.raises(ValueError):
         oracle_mod.sf_forward(cfg, np.zeros(1, np.float32))
+
+
+# ---- Siddon pair (oracle/siddon_oracle.c) ----------------------------------
+from conftest import SIDDON_GOLDEN  # noqa: E402
+
+SIDDON = load_golden(SIDDON_GOLDEN)
+S_CASES = sorted(n for n in SIDDON if not n.startswith("explicit"))
+
+
+@pytest.mark.parametrize("name", S_CASES)
+def test_oracle_siddon_matches_reference(siddon_golden, oracle_mod, name):
+    c = siddon_golden[name]
+    np.testing.assert_array_equal(oracle_mod.siddon_forward(c["config"], c["x"]), c["fwd"])
+    np.testing.assert_array_equal(oracle_mod.siddon_back(c["config"], c["y"]), c["back"])
