@@ -32,9 +32,6 @@
 #ifndef CTP_BK_MINB
 #define CTP_BK_MINB 4  // resident CTAs/SM the back kernel is register-budgeted for
 #endif
-#ifndef CTP_BK_QUNROLL
-#define CTP_BK_QUNROLL 1  // row-sum loop unroll (loads in flight per lane)
-#endif
 #ifndef CTP_FW_MINB
 #define CTP_FW_MINB 3
 #endif
@@ -91,11 +88,14 @@ __device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&
 #endif
 constexpr int BK_WARPS = CTP_BK_WARPS;  // warps per CTA (a 4 x BK_WARPS/4 block of voxel columns)
 constexpr int BK_ZPL = CTP_BK_ZPL;      // voxels per lane
-static_assert(BK_WARPS % 4 == 0, "CTAs cover 4 x BK_WARPS/4 voxel columns");
+#ifndef CTP_BK_CX
+#define CTP_BK_CX 1
+#endif
+constexpr int BK_CX = CTP_BK_CX;  // voxel columns along x per CTA (BK_WARPS / BK_CX along y)
+static_assert(BK_WARPS % BK_CX == 0, "CTAs cover BK_CX x BK_WARPS/BK_CX voxel columns");
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
 constexpr int BK_QMAX = BK_ZC * 15 / 8 + 0;  // per-warp row-sum table (rows): ZC * 1.8 + margin
 constexpr int BK_NCF = 4;           // footprint columns handled by the table path
-constexpr int BK_QUNROLL = CTP_BK_QUNROLL;  // row-sum loop unroll
 
 struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
   float A, B, E, lxy;
@@ -313,9 +313,9 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
   __shared__ __align__(16) float qbuf[BK_WARPS][BK_QMAX + 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nbx = (gp.nx + 3) >> 2;
-  const int ix = (blockIdx.x % nbx) * 4 + (warp & 3);
-  const int iy = (blockIdx.x / nbx) * (BK_WARPS / 4) + (warp >> 2);
+  const int nbx = (gp.nx + BK_CX - 1) / BK_CX;
+  const int ix = (blockIdx.x % nbx) * BK_CX + (warp % BK_CX);
+  const int iy = (blockIdx.x / nbx) * (BK_WARPS / BK_CX) + (warp / BK_CX);
   if (ix >= gp.nx || iy >= gp.ny) return;  // warp-uniform; no CTA barriers below
   const int b = blockIdx.z;
   const int izs = blockIdx.y * BK_ZC;
@@ -874,7 +874,6 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
   FvSmem& S = reinterpret_cast<FvSmem*>(smem_raw)[warp];
   const long long task = task0 + (long long)blockIdx.x * FV_WARPS + warp;
   if (task >= ntasks) return;  // warp-uniform; no CTA barriers in this kernel
-  const int nbands = (gp.nr + FW_ROWS - 1) / FW_ROWS;
   const int ntiles = (gp.nc + FW_CW - 1) / FW_CW;
   // band-major task order: consecutive CTAs sweep views and tiles of one row
   // band, i.e. the same z-range of the volume, which then stays in L2
@@ -1299,7 +1298,7 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
                         int batch, bool accumulate, cudaStream_t st) {
-  const int nbx = (gp.nx + 3) / 4, nby = (gp.ny + BK_WARPS / 4 - 1) / (BK_WARPS / 4);
+  const int nbx = (gp.nx + BK_CX - 1) / BK_CX, nby = (gp.ny + BK_WARPS / BK_CX - 1) / (BK_WARPS / BK_CX);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = min(65535, batch - b0);
     const dim3 grid(nbx * nby, (gp.nz + BK_ZC - 1) / BK_ZC, nb);
