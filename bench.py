@@ -227,7 +227,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="batch size (default: 64 for c2, else 1)")
@@ -355,10 +355,14 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        calls = []
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
+            ta = time.perf_counter()
             yo = ct.forward(shard_pair, xh)       # host in -> host out
+            tb = time.perf_counter()
             xo = ct.adjoint(shard_pair, yh)       # host in -> host out (partial volume)
+            calls.append([round((tb - ta) * 1e3, 1), round((time.perf_counter() - tb) * 1e3, 1)])
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         if world > 1:
@@ -368,7 +372,7 @@ def main():
         e2e = {"value": 2.0 * B * nvox * g.numViews * args.e2e_steps / te / 1e9, "unit": "GUPS",
                "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 4),
                "d2h_bytes_per_step": int(yo.numel() * 4 + xo.numel() * 4),
-               "steps": args.e2e_steps,
+               "steps": args.e2e_steps, "calls_ms": calls,
                "path": "paper_2307_05801_b200.forward/adjoint on pinned host tensors "
                        "(view-chunked H2D/compute/D2H overlap)"}
         if world > 1:

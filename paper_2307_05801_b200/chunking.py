@@ -34,7 +34,7 @@ import os
 from . import _native
 
 #: target bytes of sinogram per chunk (host<->device granularity)
-CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(1 << 30)))
+CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
 
 
 def _torch():
@@ -48,7 +48,7 @@ def view_chunks(nv: int, view_bytes: int, chunk_bytes: int = CHUNK_BYTES):
     32 views or more are whole multiples of 32: the back kernel sets up 32
     views per lane-parallel pass, so a ragged chunk would idle lanes."""
     per = max(1, min(nv, chunk_bytes // max(1, view_bytes)))
-    if per >= 32 and per < nv:
+    if 32 <= per < nv:
         per = per // 32 * 32
     else:
         n = math.ceil(nv / per)
@@ -77,12 +77,17 @@ def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CH
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     src = host if host.is_pinned() else host.pin_memory()
+    # one device buffer for the whole sinogram (chunks are slices of it when
+    # B == 1, where a view range is contiguous): no per-chunk allocations, so
+    # repeated calls reuse the same caching-allocator blocks
+    whole = B == 1
     with torch.cuda.device(dev):
         if direction == 0:
             out = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, pin_memory=True)
             xd = src.to(dev, non_blocking=True)
+            yall = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, device=dev) if whole else None
             for (a, e), p in zip(ranges, plans):
-                yd = p.forward(xd)
+                yd = p.forward(xd, out=yall[:, a:e]) if whole else p.forward(xd)
                 ev = torch.cuda.Event()
                 ev.record(compute)
                 copy.wait_event(ev)
@@ -91,19 +96,26 @@ def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CH
                         out.copy_(yd, non_blocking=True)
                     else:
                         out[:, a:e].copy_(yd, non_blocking=True)
-                    yd.record_stream(copy)
+                    if not whole:
+                        yd.record_stream(copy)
             compute.wait_stream(copy)
             compute.synchronize()
             return out
         out_d = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, device=dev)
+        yall = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, device=dev) if whole else None
         for k, ((a, e), p) in enumerate(zip(ranges, plans)):
             with torch.cuda.stream(copy):
                 part = src if len(ranges) == 1 else src[:, a:e]
-                yd = part.to(dev, non_blocking=True).contiguous()
+                if whole:
+                    yd = yall[:, a:e]
+                    yd.copy_(part, non_blocking=True)
+                else:
+                    yd = part.to(dev, non_blocking=True).contiguous()
             ev = torch.cuda.Event()
             ev.record(copy)
             compute.wait_event(ev)
-            yd.record_stream(compute)
+            if not whole:
+                yd.record_stream(compute)
             p.back(yd, out=out_d, accumulate=k > 0)
         out = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, pin_memory=True)
         out.copy_(out_d, non_blocking=True)
