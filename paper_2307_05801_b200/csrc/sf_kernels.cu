@@ -33,7 +33,7 @@
 #define CTP_BK_MINB 4  // resident CTAs/SM the back kernel is register-budgeted for
 #endif
 #ifndef CTP_FW_MINB
-#define CTP_FW_MINB 3
+#define CTP_FW_MINB 4
 #endif
 
 namespace ctp {
@@ -683,10 +683,23 @@ __device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& g
 constexpr int FV_WARPS = CTP_FV_WARPS;
 constexpr int FV_EBUF = 96;  // >= 31 pending + 64 from one setup round
 
+#ifndef CTP_FW_CPASYNC
+#define CTP_FW_CPASYNC 1  // prefetch x with cp.async into shared memory (vector path)
+#endif
 struct FvSmem {
   FwEntry ent[FV_EBUF];
   float xs[FW_XLEN];  // staged amp * x of one entry (or one piece)
+#if CTP_FW_CPASYNC
+  float xr[2][FW_XCAP];  // raw x of the next fast entries, filled by cp.async
+#endif
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 size_t forward_warp_smem_bytes() { return sizeof(FvSmem) * FV_WARPS; }
 
@@ -727,11 +740,29 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
   const float rbase = (float)(rw0 + lane);
   // software pipeline: x of the next fast-path entry is in flight while the
   // current entry is gathered
-  float4 xv[FW_NLD];
+  constexpr bool ASYNC = VEC && CTP_FW_CPASYNC;
+#if CTP_FW_CPASYNC
+  int pbuf = 0;  // xr buffer the next prefetch goes to
+#endif
+  float4 xv[FW_NLD];  // (register prefetch; unused, hence free, on the cp.async path)
   auto next_fast = [&](int e) {
     for (; e < nent; ++e) {
       if (S.ent[e].info & (1 << 17)) {
-        fw_prefetch<VEC>(xv, xb + ((size_t)(unsigned)S.ent[e].col << (VEC ? 2 : 0)), S.ent[e].nst, lane);
+        const float* xc = xb + ((size_t)(unsigned)S.ent[e].col << (VEC ? 2 : 0));
+#if CTP_FW_CPASYNC
+        if constexpr (ASYNC) {
+          const int nst = S.ent[e].nst;
+#pragma unroll
+          for (int t = 0; t < FW_NLD; ++t) {
+            const int s = 4 * lane + 128 * t;
+            if (s < nst) cp_async16(&S.xr[pbuf][s], xc + s);
+          }
+          cp_async_commit();
+          pbuf ^= 1;
+          return e;
+        }
+#endif
+        fw_prefetch<VEC>(xv, xc, S.ent[e].nst, lane);
         return e;
       }
     }
@@ -751,6 +782,14 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
 #pragma unroll
     for (int cc = 0; cc < FW_CW; ++cc) ts[cc] = E.ts[cc];
     if (e == e_pf) {
+#if CTP_FW_CPASYNC
+      const float* xraw = nullptr;
+      if constexpr (ASYNC) {
+        cp_async_wait_all();  // this lane's copies; the warp barrier publishes the others'
+        __syncwarp();
+        xraw = S.xr[pbuf ^ 1];
+      }
+#endif
       // stage xa = amp * x of slices za4 .. za4 + nst - 1 (4 per lane and load),
       // FW_SG loads per branch so their chains interleave
 #pragma unroll
@@ -765,8 +804,14 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
           const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
           const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
           const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
-          const float2 xaA = mul2_(ampA, make_float2(xv[t].x, xv[t].y));
-          const float2 xaB = mul2_(ampB, make_float2(xv[t].z, xv[t].w));
+          float4 xq;
+#if CTP_FW_CPASYNC
+          if constexpr (ASYNC) xq = *reinterpret_cast<const float4*>(xraw + s);
+          else
+#endif
+            xq = xv[t];
+          const float2 xaA = mul2_(ampA, make_float2(xq.x, xq.y));
+          const float2 xaB = mul2_(ampB, make_float2(xq.z, xq.w));
           if (s < nst) *reinterpret_cast<float4*>(xs + FW_XPAD + s) = make_float4(xaA.x, xaA.y, xaB.x, xaB.y);
         }
       }
