@@ -94,7 +94,10 @@ constexpr int BK_ZPL = CTP_BK_ZPL;      // voxels per lane
 constexpr int BK_CX = CTP_BK_CX;  // voxel columns along x per CTA (BK_WARPS / BK_CX along y)
 static_assert(BK_WARPS % BK_CX == 0, "CTAs cover BK_CX x BK_WARPS/BK_CX voxel columns");
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
-constexpr int BK_QMAX = BK_ZC * 15 / 8 + 0;  // per-warp row-sum table (rows): ZC * 1.8 + margin
+#ifndef CTP_BK_QMAX
+#define CTP_BK_QMAX (BK_ZC * 25 / 16)  // rows covered by slices with B <= 1.5 (+ margin)
+#endif
+constexpr int BK_QMAX = CTP_BK_QMAX;  // per-warp row-sum table (rows) for the fast path
 constexpr int BK_NCF = 4;           // footprint columns handled by the table path
 
 struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
@@ -109,6 +112,11 @@ struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
   int pad[2];
 };
 static_assert(sizeof(BkEntry) == 64, "BkEntry layout");
+
+struct BkSmem {
+  BkEntry ents[BK_WARPS][32][2];       // lane-parallel setup of 32 views, per warp
+  float qbuf[BK_WARPS][BK_QMAX + 8];   // per-warp row-sum table Q(r)
+};
 
 __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const GridParams& gp,
                                            int izs, int ize) {
@@ -310,8 +318,10 @@ __device__ __noinline__ bool back_setup(const GridParams& gp, const ViewCoef* __
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
     float* __restrict__ out, int accumulate) {
-  __shared__ __align__(16) BkEntry ents[BK_WARPS][32][2];
-  __shared__ __align__(16) float qbuf[BK_WARPS][BK_QMAX + 8];
+  extern __shared__ __align__(16) unsigned char bk_smem_raw[];
+  BkSmem& SM = *reinterpret_cast<BkSmem*>(bk_smem_raw);
+  auto& ents = SM.ents;
+  auto& qbuf = SM.qbuf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbx = (gp.nx + BK_CX - 1) / BK_CX;
   const int ix = (blockIdx.x % nbx) * BK_CX + (warp % BK_CX);
@@ -1343,14 +1353,17 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
                         int batch, bool accumulate, cudaStream_t st) {
+  cudaError_t ea = cudaFuncSetAttribute(sf_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BkSmem));
+  if (ea != cudaSuccess) return ea;
   const int nbx = (gp.nx + BK_CX - 1) / BK_CX, nby = (gp.ny + BK_WARPS / BK_CX - 1) / (BK_WARPS / BK_CX);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = min(65535, batch - b0);
     const dim3 grid(nbx * nby, (gp.nz + BK_ZC - 1) / BK_ZC, nb);
     const size_t sino_elems = (size_t)gp.nv * gp.nr * gp.nc;
     const size_t vol_elems = (size_t)gp.nx * gp.ny * gp.nz;
-    sf_back_kernel<<<grid, BK_WARPS * 32, 0, st>>>(gp, vcoef, yT + (size_t)b0 * sino_elems,
-                                                   vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0);
+    sf_back_kernel<<<grid, BK_WARPS * 32, sizeof(BkSmem), st>>>(gp, vcoef, yT + (size_t)b0 * sino_elems,
+                                                                vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0);
   }
   return cudaGetLastError();
 }
