@@ -4,7 +4,7 @@ import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2307_05801_b200 as ct
-from paper_2307_05801_b200 import configs, chunking, partition
+from paper_2307_05801_b200 import configs, partition
 
 g, spec = ct.parse_config(json.dumps(configs.C3))
 P = ct.ProjectorPair(ct.SF, g, spec)
