@@ -250,8 +250,11 @@ __global__ void __launch_bounds__(256) siddon_rays_kernel(SiddonParams p, const 
   rays[idx] = sample_ray(p, poses + 15 * view, row, col);
 }
 
+#ifndef CTP_SD_MINB
+#define CTP_SD_MINB 4  // 64 registers: occupancy hides the ray-table and division latency
+#endif
 template <bool TABLE>
-__global__ void __launch_bounds__(256) siddon_back_kernel(SiddonParams p, const double* __restrict__ poses,
+__global__ void __launch_bounds__(256, CTP_SD_MINB) siddon_back_kernel(SiddonParams p, const double* __restrict__ poses,
                                                           const Ray* __restrict__ rays,
                                                           const float* __restrict__ sino,
                                                           float* __restrict__ vol, int accumulate) {
