@@ -217,7 +217,10 @@ __device__ __forceinline__ bool project_center(const SiddonParams& p, const doub
   return true;
 }
 
-__global__ void __launch_bounds__(256) siddon_forward_kernel(SiddonParams p, const double* __restrict__ poses,
+#ifndef CTP_SDF_MINB
+#define CTP_SDF_MINB 4
+#endif
+__global__ void __launch_bounds__(256, CTP_SDF_MINB) siddon_forward_kernel(SiddonParams p, const double* __restrict__ poses,
                                                              const float* __restrict__ vol,
                                                              float* __restrict__ sino, int accumulate) {
   const long long nray = (long long)p.nv * p.nr * p.nc;
