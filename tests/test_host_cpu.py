@@ -221,3 +221,6 @@ def test_capi_validates_before_touching_the_device():
     # forward with a null plan is rejected, not crashed
     assert lib.ctp_sf_forward(None, None, None, 1, None, 0, 0, None) == 1
     assert lib.ctp_sf_workspace_bytes(None, 0, 1) == 0
+    # the Siddon entry points validate the same way
+    assert lib.ctp_siddon_forward(None, 1.0, None, None, 1, 0, None) == 1
+    assert lib.ctp_siddon_back(None, 1.0, None, None, 1, 0, None) == 1
