@@ -349,7 +349,7 @@ def main():
         shard_pair = sharded.shard
         # warm: plans, and the pinned-output pool in its steady state (a loop
         # holds the previous step's results while the next step allocates)
-        for _ in range(2):
+        for _ in range(3):
             yo = ct.forward(shard_pair, xh)
             xo = ct.adjoint(shard_pair, yh)
         torch.cuda.synchronize()

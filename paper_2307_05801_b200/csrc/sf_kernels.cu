@@ -1057,6 +1057,9 @@ __device__ __forceinline__ float row0_weight(float A, float B, float E, bool& hi
   return add_(upper, -lower);
 }
 
+#ifndef CTP_FB_ALONG_Y
+#define CTP_FB_ALONG_Y 1
+#endif
 template <int G>
 __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const ViewCoef* __restrict__ vcoef,
                                                           const float* __restrict__ yB,  // [nv][nc][Bs]
@@ -1064,9 +1067,16 @@ __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const V
                                                           int Bs, int b0, int nb) {
   __shared__ __align__(16) BkEntry ents[8][32][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if CTP_FB_ALONG_Y
+  // the CTA's 8 warps: 8 consecutive pixels along y (shared detector columns)
+  const int ix = blockIdx.x % gp.nx, iy = (blockIdx.x / gp.nx) * 8 + warp;
+  if (iy >= gp.ny) return;
+  const int pix = iy * gp.nx + ix;
+#else
   const int pix = blockIdx.x * 8 + warp;
   if (pix >= gp.nx * gp.ny) return;
   const int ix = pix % gp.nx, iy = pix / gp.nx;
+#endif
   BkEntry(&my)[32][2] = ents[warp];
   float acc[G];
 #pragma unroll
@@ -1231,6 +1241,9 @@ __device__ __noinline__ int fan_candidates(const GridParams& gp, const ViewCoef*
   return __shfl_sync(0xffffffffu, ni, 31);
 }
 
+#ifndef CTP_FF_VIEWS_FAST
+#define CTP_FF_VIEWS_FAST 1
+#endif
 template <int G>
 __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xB,  // [ny*nx][Bs]
@@ -1242,8 +1255,15 @@ __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
   const int ntiles = (gp.nc + FW_CW - 1) / FW_CW;
   const long long task = (long long)blockIdx.x * FV_WARPS + warp;
   if (task >= (long long)ntiles * gp.nv) return;
+#if CTP_FF_VIEWS_FAST
+  // consecutive warps: the same tile in consecutive views (their wedges, and
+  // the pixels' batch rows they read, nearly coincide -> L1 reuse)
+  const int tile = (int)(task / gp.nv);
+  const int v = (int)(task % gp.nv);
+#else
   const int tile = (int)(task % ntiles);
   const int v = (int)(task / ntiles);
+#endif
   const int c0 = tile * FW_CW;
   const int cw = min(FW_CW, gp.nc - c0);
   const ViewCoef vc = vcoef[v];
@@ -1418,7 +1438,11 @@ cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, cons
 
 cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
                             int batch, cudaStream_t st) {
+#if CTP_FB_ALONG_Y
+  const unsigned grid = (unsigned)(gp.nx * ((gp.ny + 7) / 8));
+#else
   const unsigned grid = (unsigned)((gp.nx * gp.ny + 7) / 8);
+#endif
   for (int b0 = 0; b0 < batch; b0 += 32 * F2_MAXG) {
     const int nb = min(32 * F2_MAXG, batch - b0);
     const int G = (nb + 31) / 32;
