@@ -114,7 +114,8 @@ struct BkEntry {  // one (sub-)voxel footprint of the warp's column in one view
 static_assert(sizeof(BkEntry) == 64, "BkEntry layout");
 
 struct BkSmem {
-  BkEntry ents[BK_WARPS][32][2];       // lane-parallel setup of 32 views, per warp
+  BkEntry ents[BK_WARPS][32];          // lane-parallel setup of 32 views, per warp
+  BkEntry split[BK_WARPS];             // second sub-footprint of a split voxel (rare)
   float qbuf[BK_WARPS][BK_QMAX + 8];   // per-warp row-sum table Q(r)
 };
 
@@ -315,6 +316,27 @@ __device__ __noinline__ bool back_setup(const GridParams& gp, const ViewCoef* __
   return split;
 }
 
+// 3D back kernel variant of back_setup: only the first sub-footprint is kept
+// (its mask in pad[0]); the second one of a split voxel is rebuilt in the
+// view loop when needed, which halves the entry table (more L1 for y rows)
+__device__ __noinline__ bool back_setup1(const GridParams& gp, const ViewCoef* __restrict__ vcoef, int vb,
+                                         int ix, int iy, int izs, int ize, BkEntry* e) {
+  const int v = vb + (threadIdx.x & 31);
+  BkEntry e0;
+  e0.ncol = 0;
+  e0.pk = 0;
+  int mask = 0;
+  if (v < gp.nv) {
+    const ViewCoef vc = vcoef[v];
+    SubFoot f0, f1;
+    mask = column_footprint(vc, gp, ix, iy, f0, f1);
+    if (mask & 1) fill_entry(e0, f0, gp, izs, ize);
+  }
+  e0.pad[0] = mask;
+  *e = e0;
+  return __any_sync(0xffffffffu, (mask & 2) != 0);
+}
+
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
     float* __restrict__ out, int accumulate) {
@@ -334,7 +356,8 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   const size_t view_elems = (size_t)nc * nr;
   const float* yb = yT + (size_t)b * gp.nv * view_elems;
   float* qw = qbuf[warp];
-  BkEntry(&my)[32][2] = ents[warp];
+  BkEntry(&my)[32] = ents[warp];
+  BkEntry& sp = SM.split[warp];
   // this lane's slices: izs + lane + 32 m, m < nvalid
   const int span = ize - izs - lane;  // may be negative when nz < 32
   const int nvalid = span < 0 ? 0 : min(BK_ZPL, span / 32 + 1);
@@ -346,14 +369,23 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   for (int vb = 0; vb < gp.nv; vb += 32) {
     // ---- lane-parallel footprint setup: lane l <- view vb + l
     // nsub = 2 when any view of this batch splits the voxel (_sf_subdivide), else 1
-    const int nsub = back_setup(gp, vcoef, vb, ix, iy, izs, ize, &my[lane][0]) ? 2 : 1;
+    const int nsub = back_setup1(gp, vcoef, vb, ix, iy, izs, ize, &my[lane]) ? 2 : 1;
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
     const float* yview = yb + (size_t)vb * view_elems;  // [c][r] of view vb + j
     for (int j = 0; j < nvb; ++j, yview += view_elems) {
 #pragma unroll 1
       for (int s = 0; s < nsub; ++s) {
-        const BkEntry& ef = my[j][s];
+        if (s == 1) {  // the second half of a split voxel (_sf_subdivide), rebuilt
+          if (!(my[j].pad[0] & 2)) continue;
+          if (lane == 0) {
+            SubFoot f0, f1;
+            column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
+            fill_entry(sp, f1, gp, izs, ize);
+          }
+          __syncwarp();
+        }
+        const BkEntry& ef = s == 0 ? my[j] : sp;
         const int pk = ef.pk;
         if (pk & 1) {
           // fast path: everything precomputed; 4-row float4 row sums, then slices
