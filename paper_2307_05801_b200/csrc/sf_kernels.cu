@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
       for (int s = 0; s < nsub; ++s) {
         if (s == 1) {  // the second half of a split voxel (_sf_subdivide), rebuilt
           if (!(my[j].pad[0] & 2)) continue;
+          __syncwarp();  // every lane is done with the previous split entry
           if (lane == 0) {
             SubFoot f0, f1;
             column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
