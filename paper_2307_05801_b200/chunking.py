@@ -63,15 +63,23 @@ def chunk_plans(plan: "_native.Plan", ranges):
     return [_native.get_plan(g.with_views(range(a, b)), spec, dev) for a, b in ranges]
 
 
-def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int = CHUNK_BYTES):
+#: at most this many view chunks per call: each chunk is one kernel launch, and
+#: a back-projection launch re-reads and re-writes the accumulated volume
+MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "8"))
+
+
+def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int | None = None):
     """Apply A (direction 0) / A^T (1) to a host f32 tensor [B, ...]; returns
     a pinned host tensor.  The whole batch moves together (so batched paths
-    such as the fan-beam kernels apply); views are chunked by bytes."""
+    such as the fan-beam kernels apply); views are chunked by bytes
+    (``CHUNK_BYTES``, or more per chunk so there are at most ``MAX_CHUNKS``)."""
     torch = _torch()
     dev = plan.device
     B = int(host.shape[0])
     nv, nr, nc = plan.sino_shape
     view_bytes = B * nr * nc * 4
+    if chunk_bytes is None:
+        chunk_bytes = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
     ranges = view_chunks(nv, view_bytes, chunk_bytes)
     plans = chunk_plans(plan, ranges)
     compute = torch.cuda.current_stream(dev)
