@@ -404,3 +404,32 @@ def test_full_size_adjoint_and_linearity(which):
     a2 = plan.forward(x2)
     err = float((a12.double() - ax.double() - a2.double()).norm() / a12.double().norm())
     assert err <= 1e-6, err
+
+
+@pytest.mark.parametrize("world", [2, 3, 6])
+def test_view_sharded_partials_on_device(world, golden):
+    """The N-rank view-sharded pair (partition.ViewShardedProjector with the
+    CUDA backend), every rank's shard run on this GPU: forward shards
+    concatenate to the single-GPU forward bitwise (views are independent),
+    and the per-rank partial volumes sum to the single-GPU back projection
+    (what the NCCL reduce-scatter computes) to fp32 reassociation."""
+    from paper_2307_05801_b200 import partition
+
+    c = golden["c3_optics"]
+    P = pair_of(c["config"])
+    nv = P.geometry.numViews
+    if world > nv:
+        pytest.skip("more ranks than views")
+    x = torch.from_numpy(c["x"])[None].to(DEV)
+    y = torch.from_numpy(c["y"])[None].to(DEV)
+    full_f = ct.forward(P, x)
+    full_b = ct.adjoint(P, y)
+    parts_f, total_b = [], None
+    for r in range(world):
+        sp = partition.ViewShardedProjector(P, r, world, device=DEV)
+        a, b = sp.views
+        parts_f.append(sp.forward(x))
+        part = sp._partial(y[:, a:b].contiguous())[:, : P.volumeSpec.numZ]
+        total_b = part.clone() if total_b is None else total_b + part
+    assert torch.equal(torch.cat(parts_f, dim=1), full_f)
+    assert rel_l2(total_b.cpu().numpy(), full_b.cpu().numpy()) <= 1e-6
