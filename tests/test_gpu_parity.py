@@ -433,3 +433,19 @@ def test_view_sharded_partials_on_device(world, golden):
         total_b = part.clone() if total_b is None else total_b + part
     assert torch.equal(torch.cat(parts_f, dim=1), full_f)
     assert rel_l2(total_b.cpu().numpy(), full_b.cpu().numpy()) <= 1e-6
+
+
+def test_c3_optics_curved_detector_subset(oracle_mod):
+    """C3 optics with a curved (cylindrical) detector on a 256^3 grid and a
+    view subset: the atan2 column map of the curved kind at scale."""
+    cfg = dict(C3, geometry="cone-curved", numX=256, numY=256, numZ=256, voxelWidth=1.3333,
+               voxelHeight=1.3333, numRows=384, numCols=384, pixelHeight=2.0, pixelWidth=2.0)
+    _parity(oracle_mod, cfg, views=[0, 133, 301, 577])
+
+
+def test_c3_optics_offsets_and_shifted_detector(oracle_mod):
+    """C3 optics with the grid off-centre and the detector centre shifted
+    (rays enter the grid obliquely at the edges, partial row windows)."""
+    cfg = dict(C3, numX=192, numY=160, numZ=128, voxelWidth=1.0, voxelHeight=1.2, offsetX=15.0,
+               offsetY=-9.0, offsetZ=11.0, numRows=300, numCols=360, centerRow=140.3, centerCol=170.8)
+    _parity(oracle_mod, cfg, views=[7, 95, 260, 640])
