@@ -636,6 +636,51 @@ __device__ __forceinline__ float fw_row_sum(const float* xs, float rf, float A, 
   return p;
 }
 
+#ifndef CTP_FW_PAIRS
+#define CTP_FW_PAIRS 1  // each lane owns two adjacent rows; they share candidate slices
+#endif
+// Two adjacent rows r, r + 1 (row coordinate rf, rf + 1).  With two candidates
+// per row (B >= 1.02), row r + 1's window starts d = 0 or 1 slices later, so
+// the pair needs slices j0 .. j0 + 2 only: T, lo / hi and xa are evaluated once
+// and row r + 1 selects its pair by d.  Every value is the one fw_row_sum<2>
+// computes for that row (same fma / add operands), so results are bitwise
+// unchanged.  Three candidates: two independent fw_row_sum<3> calls.
+template <int NC>
+__device__ __forceinline__ void fw_row_pair(const float* xs, float rf, float A, float B, float E, float invB,
+                                            float cb, int off, int hic, float& pa, float& pb) {
+  if (NC != 2) {
+    pa = fw_row_sum<NC>(xs, rf, A, B, E, invB, cb, off, hic);
+    pb = fw_row_sum<NC>(xs, add_(rf, 1.0f), A, B, E, invB, cb, off, hic);
+    return;
+  }
+  const float rf1 = add_(rf, 1.0f);
+  const float cfa = floorf(fmaf(rf, invB, cb));
+  const float cfb = floorf(fmaf(rf1, invB, cb));
+  const bool d = cfb > cfa;  // row r + 1's first candidate is j0 + 1
+  const int idx = min(max((int)cfa + off, 0), hic);
+  float rlo, rhi, rlo1, rhi1;
+  asm volatile("{.reg .b64 ra, rd;\n\tmov.b64 ra, {%2, %2};\n\tadd.rn.f32x2 rd, ra, %3;\n\tmov.b64 {%0, %1}, rd;}"
+               : "=f"(rlo), "=f"(rhi) : "f"(rf), "l"(0x3f000000bf000000ull));
+  asm volatile("{.reg .b64 ra, rd;\n\tmov.b64 ra, {%2, %2};\n\tadd.rn.f32x2 rd, ra, %3;\n\tmov.b64 {%0, %1}, rd;}"
+               : "=f"(rlo1), "=f"(rhi1) : "f"(rf1), "l"(0x3f000000bf000000ull));
+  const float j0 = add_(cfa, 1.0f);
+  const float2 T = fma2_(bc2_(B), make_float2(j0, add_(j0, 1.0f)), bc2_(A));
+  const float T2 = fma_(B, add_(j0, 2.0f), A);
+  const float2 hl = add2_(T, make_float2(E, -E));      // (hi_0, lo_1)
+  const float2 hl1 = add2_(make_float2(T.y, T2), make_float2(E, -E));  // (hi_1, lo_2)
+  const float x0 = xs[idx], x1 = xs[idx + 1], x2 = xs[idx + 2];
+  float2 ov = add2_(make_float2(fminf(hl.x, rhi), rhi), make_float2(-rlo, -fmaxf(hl.y, rlo)));
+  ov = make_float2(fmaxf(ov.x, 0.0f), fmaxf(ov.y, 0.0f));
+  const float2 pp = mul2_(ov, make_float2(x0, x1));
+  pa = add_(pp.x, pp.y);
+  const float hf = d ? hl1.x : hl.x, ll = d ? hl1.y : hl.y;
+  const float xf = d ? x1 : x0, xl = d ? x2 : x1;
+  float2 ob = add2_(make_float2(fminf(hf, rhi1), rhi1), make_float2(-rlo1, -fmaxf(ll, rlo1)));
+  ob = make_float2(fmaxf(ob.x, 0.0f), fmaxf(ob.y, 0.0f));
+  const float2 pq = mul2_(ob, make_float2(xf, xl));
+  pb = add_(pq.x, pq.y);
+}
+
 // Rows of this lane in the 32-row groups [g0, g1], FW_RG groups per step (one
 // branch per block, so the independent row chains interleave; a row outside
 // [g0, g1] inside an active block adds exactly 0):
@@ -648,22 +693,54 @@ __device__ __forceinline__ float fw_row_sum(const float* xs, float rf, float A, 
 // [0, hic]; both ends of the buffer hold >= 4 zeros, and a clamp only happens
 // for virtual slices j < 0 or j >= nz, whose xa is 0).
 #ifndef CTP_FW_RG
+#if CTP_FW_PAIRS
+#define CTP_FW_RG 2  // row slots evaluated per branch (one adjacent-row pair)
+#else
 #define CTP_FW_RG 3  // row groups evaluated per branch (independent chains that interleave)
+#endif
 #endif
 constexpr int FW_RG = CTP_FW_RG;
 static_assert(FW_KR % FW_RG == 0, "row groups are processed in blocks of FW_RG");
+
+// row of register slot kk of this lane (lane's rbase = rw0 + lane, or
+// rw0 + 2 lane with adjacent-row pairs)
+__device__ __forceinline__ float fw_row_of(float rbase, int kk) {
+#if CTP_FW_PAIRS
+  return rbase + (float)(64 * (kk >> 1) + (kk & 1));
+#else
+  return rbase + (float)(32 * kk);
+#endif
+}
+__device__ __forceinline__ int fw_row_base(int rw0, int lane) {
+#if CTP_FW_PAIRS
+  return rw0 + 2 * lane;
+#else
+  return rw0 + lane;
+#endif
+}
 
 template <int NC>
 __device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float (&ts)[FW_CW],
                                         const float* xs, float rbase, float A, float B, float E,
                                         float invB, float cb, int off, int hic, int g0, int g1) {
+#if CTP_FW_PAIRS
+  static_assert(FW_RG % 2 == 0, "row pairs need an even FW_RG");
+  g0 &= ~1;  // 32-row groups -> register slots: slot pair (2q, 2q+1) covers groups 2q, 2q+1
+  g1 |= 1;
+#endif
 #pragma unroll
   for (int kk = 0; kk < FW_KR; kk += FW_RG) {
     if (kk + FW_RG - 1 < g0 || kk > g1) continue;  // warp-uniform
     float p[FW_RG];
+#if CTP_FW_PAIRS
+#pragma unroll
+    for (int q = 0; q < FW_RG; q += 2)
+      fw_row_pair<NC>(xs, fw_row_of(rbase, kk + q), A, B, E, invB, cb, off, hic, p[q], p[q + 1]);
+#else
 #pragma unroll
     for (int q = 0; q < FW_RG; ++q)
-      p[q] = fw_row_sum<NC>(xs, rbase + (float)(32 * (kk + q)), A, B, E, invB, cb, off, hic);
+      p[q] = fw_row_sum<NC>(xs, fw_row_of(rbase, kk + q), A, B, E, invB, cb, off, hic);
+#endif
 #pragma unroll
     for (int cc = 0; cc < FW_CW; cc += 2) {
       const float2 t2 = make_float2(ts[cc], ts[cc + 1]);
@@ -780,7 +857,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
                                            const GridParams& gp, const float* __restrict__ xb,
                                            int rw0, int lane) {
   float* xs = S.xs;
-  const float rbase = (float)(rw0 + lane);
+  const float rbase = (float)fw_row_base(rw0, lane);
   // software pipeline: x of the next fast-path entry is in flight while the
   // current entry is gathered
   constexpr bool ASYNC = VEC && CTP_FW_CPASYNC;
@@ -886,9 +963,14 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
       }
       __syncwarp();
 #pragma unroll
+#if CTP_FW_PAIRS
+      const int k0 = g0 & ~1, k1 = g1 | 1;
+#else
+      const int k0 = g0, k1 = g1;
+#endif
       for (int kk = 0; kk < FW_KR; ++kk) {
-        if (kk < g0 || kk > g1) continue;
-        const float rf = rbase + (float)(32 * kk);
+        if (kk < k0 || kk > k1) continue;
+        const float rf = fw_row_of(rbase, kk);
         const float rlo = sub_(rf, 0.5f), rhi = add_(rf, 0.5f);
         const int c = (int)floorf(fmaf(rf, invB, cb));
         const int j1 = min(c + nc, pe);
@@ -1054,7 +1136,7 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
 #pragma unroll
   for (int kk = 0; kk < FW_KR; ++kk) {
-    const int r = rw0 + 32 * kk + lane;
+    const int r = (int)fw_row_of((float)fw_row_base(rw0, lane), kk);
     if (r > rw1) continue;
     float* row = yv + (size_t)r * gp.nc + c0;
 #pragma unroll
