@@ -19,6 +19,7 @@
 #include "sf_launch.h"
 
 using ctp::GridParams;
+using ctp::ViewAx;
 using ctp::ViewCoef;
 
 struct ctp_plan {
@@ -26,8 +27,9 @@ struct ctp_plan {
   std::vector<double> poses;   // host copy, nv*15
   int device;
   ViewCoef* d_coef;            // device, nv entries
+  ViewAx* d_ax;                // device, nv entries (f64 axial map of the 3D kernels)
   double* d_pose;              // device, nv*15 float64 (Siddon pair)
-  bool sf_ok;                  // SF supports this geometry (SF-modular needs rowDir.z > 0.05)
+  bool sf_ok;                  // SF supports this geometry (SF-modular: upright panels only)
   std::string sf_reason;
   GridParams gp;
   size_t vol_elems, sino_elems;
@@ -91,23 +93,38 @@ int validate(const ctp_geom* g) {
   return CTP_OK;
 }
 
-// the SF-modular model keeps detector rows increasing with z (the Siddon pair
-// has no such restriction, so this is checked per model, not per plan)
+// SF-modular (an extension: the reference raises UnsupportedGeometryError for
+// SF + modular, sf.py:23-27) is exact only for UPRIGHT panels: detector
+// columns horizontal (colDir.z = 0) and rows vertical (rowDir = +z), in any
+// position and yaw, with the source anywhere.  Then the detector normal is
+// horizontal, a voxel column's transverse footprint does not move with z and
+// its axial map is affine in z, exactly as for cone-flat.  A tilted panel
+// would need a z-dependent transverse footprint (non-separable), so it is
+// rejected here instead of being approximated; the Siddon pair supports every
+// modular pose.
+constexpr double kUprightTol = 1e-6;
 bool sf_supports(const ctp_geom* g) {
   if (g->kind != CTP_MODULAR) return true;
-  for (int v = 0; v < g->num_views; ++v)
-    if (!(g->poses[15 * v + 11] > 0.05)) return false;
+  for (int v = 0; v < g->num_views; ++v) {
+    const double* P = g->poses + 15 * v;
+    const double uz = P[8], vx = P[9], vy = P[10], vz = P[11];
+    if (!(std::fabs(uz) <= kUprightTol && std::fabs(vx) <= kUprightTol && std::fabs(vy) <= kUprightTol &&
+          vz > 0.0))
+      return false;
+  }
   return true;
 }
 
 // float64 digestion of one view's pose into affine footprint coefficients
 // over centred grid-index coordinates (see sf_common.cuh for the frame).
-void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>& out) {
+void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>& out,
+                      std::vector<ViewAx>& axo) {
   const double hx = g.voxel_width, hz = g.voxel_height;
   const double pw = g.pixel_width, ph = g.pixel_height, cr = g.center_row, cc = g.center_col;
   const double xm = g.x0 + 0.5 * g.num_x * hx, ym = g.y0 + 0.5 * g.num_y * hx;
   const double half_x = 0.5 * g.num_x, half_y = 0.5 * g.num_y;
   out.assign(g.num_views, ViewCoef{});
+  axo.assign(g.num_views, ViewAx{});
   for (int v = 0; v < g.num_views; ++v) {
     const double* s = P + 15 * v;
     const double* c0 = s + 3;
@@ -115,6 +132,7 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
     const double* vax = s + 9;
     const double* w = s + 12;
     ViewCoef& c = out[v];
+    ViewAx& ax = axo[v];
     c.ux = (float)u[0];
     c.uy = (float)u[1];
     c.wx = (float)w[0];
@@ -136,6 +154,12 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
       c.tc = (float)(hx * vax[1] / ph);
       c.tz = (float)(hz * vax[2] / ph);
       c.cull = 1;
+      ax.k0 = 1.0;  // mag = 1
+      ax.lam = 1.0;
+      ax.a0 = ((xm - c0[0]) * vax[0] + (ym - c0[1]) * vax[1] + (g.z0 + 0.5 * hz - c0[2]) * vax[2]) / ph + cr;
+      ax.a2 = hx * vax[0] / ph;
+      ax.a3 = hx * vax[1] / ph;
+      ax.bz = hz * vax[2] / ph;
       continue;
     }
     if (g.kind == CTP_MODULAR) {
@@ -169,6 +193,15 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
       const bool inside = std::fabs((s[0] - xm) / hx) < half_x + 2.0 &&
                           std::fabs((s[1] - ym) / hx) < half_y + 2.0;
       c.cull = inside ? 0 : 1;
+      ax.k0 = (xm - s[0]) * nxv + (ym - s[1]) * nyv + (zr - s[2]) * nzv;
+      ax.k1 = hx * nxv;
+      ax.k2 = hx * nyv;
+      ax.lam = lamnum;
+      ax.a0 = ((s[0] - c0[0]) * vax[0] + (s[1] - c0[1]) * vax[1] + (s[2] - c0[2]) * vax[2]) / ph + cr;
+      ax.a1 = vax[2] * (g.z0 + 0.5 * hz - s[2]) / ph + ((xm - s[0]) * vax[0] + (ym - s[1]) * vax[1]) / ph;
+      ax.a2 = hx * vax[0] / ph;
+      ax.a3 = hx * vax[1] / ph;
+      ax.bz = vax[2] * hz / ph;
       continue;
     }
     // cone: plane normal and lamnum (_kernels.py:562-569)
@@ -190,6 +223,10 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
       c.s0 = (float)(((s[0] - c0[0]) * u[0] + (s[1] - c0[1]) * u[1] + (s[2] - c0[2]) * u[2]) / pw + cc);
       c.g = (float)(lamnum / pw);
       c.lamnum = (float)lamnum;
+      ax.k0 = (xm - s[0]) * nxv + (ym - s[1]) * nyv;
+      ax.k1 = hx * nxv;
+      ax.k2 = hx * nyv;
+      ax.lam = lamnum;
     } else {  // curved: s = sdd * atan2(e.u, e.w) (_kernels.py:478-497)
       c.na = (float)((xm - s[0]) * u[0] + (ym - s[1]) * u[1]);
       c.nb = (float)(hx * u[0]);
@@ -200,7 +237,15 @@ void build_view_coefs(const ctp_geom& g, const double* P, std::vector<ViewCoef>&
       c.s0 = (float)cc;
       c.g = (float)(g.sdd / pw);
       c.lamnum = (float)g.sdd;
+      ax.k0 = xm - s[0];
+      ax.k1 = ym - s[1];
+      ax.k2 = hx;
+      ax.lam = g.sdd;
     }
+    // cone axial map: tcen = mag (cz - src_z) (_kernels.py:626-628) in row units
+    ax.a0 = cr;
+    ax.a1 = (g.z0 + 0.5 * hz - s[2]) / ph;
+    ax.bz = hz / ph;
     // wedge culling assumes the source lies outside the grid footprint
     const bool inside = std::fabs((s[0] - xm) / hx) < half_x + 2.0 &&
                         std::fabs((s[1] - ym) / hx) < half_y + 2.0;
@@ -308,18 +353,22 @@ int ctp_plan_create(const ctp_geom* geom, int device, ctp_plan** plan_out) {
   p->vol_elems = (size_t)geom->num_x * geom->num_y * geom->num_z;
   p->sino_elems = (size_t)geom->num_views * geom->num_rows * geom->num_cols;
   std::vector<ViewCoef> coefs;
-  build_view_coefs(*geom, p->poses.data(), coefs);
+  std::vector<ViewAx> axs;
+  build_view_coefs(*geom, p->poses.data(), coefs, axs);
   cudaError_t e = cudaMalloc(&p->d_coef, sizeof(ViewCoef) * coefs.size());
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(view coefficients)");
   }
   e = cudaMemcpy(p->d_coef, coefs.data(), sizeof(ViewCoef) * coefs.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_ax, sizeof(ViewAx) * axs.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_ax, axs.data(), sizeof(ViewAx) * axs.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_pose, sizeof(double) * p->poses.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(p->d_pose, p->poses.data(), sizeof(double) * p->poses.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(p->d_coef);
+    if (p->d_ax) cudaFree(p->d_ax);
     if (p->d_pose) cudaFree(p->d_pose);
     delete p;
     return cuda_fail(e, "upload view tables");
@@ -333,6 +382,7 @@ int ctp_plan_destroy(ctp_plan* plan) {
   if (!plan) return CTP_OK;
   DeviceGuard guard(plan->device);
   if (plan->d_coef) cudaFree(plan->d_coef);
+  if (plan->d_ax) cudaFree(plan->d_ax);
   if (plan->d_pose) cudaFree(plan->d_pose);
   for (int d = 0; d < 2; ++d)
     for (int k = 0; k < 2; ++k)
@@ -364,7 +414,8 @@ size_t ctp_sf_workspace_bytes(const ctp_plan* plan, int direction, int batch) {
 static int check_sf(const ctp_plan* plan) {
   if (plan && !plan->sf_ok)
     return fail(CTP_ERR_UNSUPPORTED_GEOMETRY,
-                "SF-modular needs rowDir with a positive z component (> 0.05) in every view");
+                "SF-modular needs upright detector panels (colDir.z == 0, rowDir == +z) in every view; "
+                "use the Siddon model for tilted panels");
   return CTP_OK;
 }
 
@@ -395,7 +446,7 @@ int ctp_sf_forward(const ctp_plan* plan, const float* vol, float* sino, int batc
   cudaError_t e = ctp::launch_transpose(vol, xT, gp.nz, gp.nx * gp.ny, batch, s);
   if (e != cudaSuccess) return cuda_fail(e, "transpose volume");
   KernelTimer timer(plan, 0, s, flags);
-  e = ctp::launch_forward(gp, plan->d_coef, xT, sino, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  e = ctp::launch_forward(gp, plan->d_coef, plan->d_ax, xT, sino, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
   timer.stop();
   if (e != cudaSuccess) return cuda_fail(e, "sf_forward_kernel");
   return CTP_OK;
@@ -428,7 +479,7 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
   cudaError_t e = ctp::launch_transpose(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
   if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram");
   KernelTimer timer(plan, 1, s, flags);
-  e = ctp::launch_back(gp, plan->d_coef, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  e = ctp::launch_back(gp, plan->d_coef, plan->d_ax, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
   timer.stop();
   if (e != cudaSuccess) return cuda_fail(e, "sf_back_kernel");
   return CTP_OK;

@@ -9,8 +9,11 @@
 // functions in this header.  Every floating-point step of the coefficient is
 // written with explicit-rounding intrinsics (__fmul_rn, __fadd_rn, __fmaf_rn,
 // ...) so that nvcc cannot contract or reassociate it differently in the two
-// kernels: the pair is then an exact transpose in fp32 (the explicit-matrix
-// test, pkg/tests/test_sf.py:89-111, holds bitwise).
+// kernels.  The fan pair shares every operand and is an exact fp32 transpose;
+// the 3D pair measures footprint edges from different local origins (the
+// forward's band row, the back's table row; see fill_entry / localize_entry)
+// and is a transpose to fp32 rounding (explicit-matrix test,
+// pkg/tests/test_sf.py:89-111, at 4e-6 of max|A|).
 //
 // Coordinates.  Geometry is pre-digested on the host in float64 (ctp_plan)
 // into per-view affine coefficients over CENTRED GRID-INDEX coordinates
@@ -60,6 +63,24 @@ struct alignas(16) ViewCoef {
   float pad[2];
 };
 static_assert(sizeof(ViewCoef) == 128, "ViewCoef must stay 128 bytes");
+
+// Per-view float64 axial map (built with ViewCoef in capi.cu).  For a voxel
+// column centred at (X, Y) (centred grid-index coords):
+//   mag = lam / den,   den = k0 + k1 X + k2 Y      (flat cone, modular, parallel: lam = k0 = 1)
+//   mag = lam / rho,   rho = |(k0 + k2 X, k1 + k2 Y)|  (curved cone: k2 = hx)
+//   A   = a0 + mag (a1 + a2 X + a3 Y)   row coordinate of slice 0's centre
+//   B   = mag bz                        rows per slice (E = B / 2)
+// i.e. exactly the axial map of _kernels.py:619-645 (tcen / ph + cr,
+// te = mag hz / 2).  The 3D kernels evaluate it in f64 once per (column,
+// view) and hand the kernels positions RELATIVE to a local origin, so fp32
+// resolves footprint edges to ~1e-5 row even on 1536-row detectors.
+struct alignas(16) ViewAx {
+  double k0, k1, k2, lam;
+  double a0, a1, a2, a3;
+  double bz;
+  double pad[3];
+};
+static_assert(sizeof(ViewAx) == 96, "ViewAx layout");
 
 // Launch-invariant scalars.
 struct GridParams {
@@ -314,6 +335,49 @@ __device__ __forceinline__ int column_footprint(const ViewCoef& v, const GridPar
   if (sub_footprint(v, gp, X0, Y0, hxi, hyi, s0)) mask |= 1;
   if (sub_footprint(v, gp, X1, Y1, hxi, hyi, s1)) mask |= 2;
   return mask;
+}
+
+// column_footprint plus the (sub-)voxel centres and a split flag (bit 2 of
+// the returned mask) for the 3D kernels, which evaluate the axial map of
+// each sub-footprint in f64 at its own centre.
+__device__ __forceinline__ int column_subs(const ViewCoef& v, const GridParams& gp, int ix, int iy,
+                                           SubFoot& s0, SubFoot& s1, float2& c0, float2& c1) {
+  const float X = sub_((float)ix + 0.5f, gp.half_x);
+  const float Y = sub_((float)iy + 0.5f, gp.half_y);
+  c0 = make_float2(X, Y);
+  c1 = c0;
+  if (!sub_footprint(v, gp, X, Y, 0.5f, 0.5f, s0)) return 0;
+  if (!(sub_(s0.t3, s0.t0) > 8.0f)) return 1;
+  const bool along_x = v.split_x != 0;
+  const float hxi = along_x ? 0.25f : 0.5f, hyi = along_x ? 0.5f : 0.25f;
+  c0 = along_x ? make_float2(sub_(X, 0.25f), Y) : make_float2(X, sub_(Y, 0.25f));
+  c1 = along_x ? make_float2(add_(X, 0.25f), Y) : make_float2(X, add_(Y, 0.25f));
+  int mask = 4;
+  if (sub_footprint(v, gp, c0.x, c0.y, hxi, hyi, s0)) mask |= 1;
+  if (sub_footprint(v, gp, c1.x, c1.y, hxi, hyi, s1)) mask |= 2;
+  return mask;
+}
+
+// 1/d to f64 precision without a full DDIV: fp32 reciprocal (~2^-23) and
+// two Newton steps in f64 (2^-46, then ~2^-52)
+__device__ __forceinline__ double rcp64(double d) {
+  double r = (double)__frcp_rn((float)d);
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+
+// f64 axial map of ViewAx at (X, Y): row coordinate A of slice 0's centre and
+// rows per slice B.
+__device__ __forceinline__ void axial64(const ViewAx& a, int kind, double X, double Y, double& A, double& B) {
+  double mag;
+  if (kind == kConeCurved) {
+    const double dx = fma(a.k2, X, a.k0), dy = fma(a.k2, Y, a.k1);
+    mag = a.lam * rcp64(sqrt(fma(dx, dx, dy * dy)));
+  } else {
+    mag = a.lam * rcp64(fma(a.k2, Y, fma(a.k1, X, a.k0)));
+  }
+  A = fma(mag, fma(a.a3, Y, fma(a.a2, X, a.a1)), a.a0);
+  B = mag * a.bz;
 }
 
 #endif  // __CUDACC__

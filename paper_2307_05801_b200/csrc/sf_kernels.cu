@@ -43,11 +43,11 @@ namespace ctp {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in,
                                                         float* __restrict__ out, int R, int C,
-                                                        int batch0) {
+                                                        int batch0, int rblock0) {
   __shared__ float tile[32][33];
   const int b = blockIdx.z + batch0;
   const size_t off = (size_t)b * (size_t)R * (size_t)C;
-  const int c_base = blockIdx.x * 32, r_base = blockIdx.y * 32;
+  const int c_base = blockIdx.x * 32, r_base = (blockIdx.y + rblock0) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
 #pragma unroll
   for (int k = 0; k < 32; k += 8) {
@@ -119,8 +119,16 @@ struct BkSmem {
   float qbuf[BK_WARPS][BK_QMAX + 8];   // per-warp row-sum table Q(r)
 };
 
-__device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const GridParams& gp,
-                                           int izs, int ize) {
+// One entry of the lane-parallel setup.  With `ax` (3D back kernel) the
+// axial map is taken in f64 at the (sub-)voxel centre and stored RELATIVE to
+// a local origin: rows counted from `origin` (= the 4-aligned first table
+// row, kept in pad[1]) and slices counted from izs, so that
+// T = A + B * (iz - izs) stays below ~B * 32 * BK_ZPL rows in magnitude and
+// fp32 resolves footprint edges to ~1e-5 row even on 1536-row detectors
+// (round 1 used absolute row coordinates: 1.2e-4 row at C5).  Without `ax`
+// (fan kernels: one slice, one row) the f32 absolute map is kept.
+__device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const GridParams& gp, int izs, int ize,
+                                           const ViewAx* ax = nullptr, float2 cxy = make_float2(0.0f, 0.0f)) {
   e.A = f.A; e.B = f.B; e.E = f.E; e.lxy = f.lxy; e.a0 = f.a0; e.a1 = f.a1;
   e.cl = f.cl;
   e.ncol = f.ch >= f.cl ? f.ch - f.cl + 1 : 0;
@@ -130,8 +138,24 @@ __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const G
 #pragma unroll
   for (int k = 0; k < BK_NCF; ++k) e.ts[k] = k < e.ncol ? ts[k] : 0.0f;
   const int K = rows_per_slice(f.B);
-  const int Ra = first_row(sub_(fma_(f.B, (float)izs, f.A), f.E));
-  const int Rz = first_row(sub_(fma_(f.B, (float)ize, f.A), f.E)) + K - 1;
+  int Ra, Rz;
+  if (ax) {
+    double A, B;
+    axial64(*ax, gp.kind, (double)cxy.x, (double)cxy.y, A, B);
+    const double Ts = fma(B, (double)izs, A), Te = fma(B, (double)ize, A);
+    Ra = (int)floor(Ts - 0.5 * B - 0.5) + 1;
+    Rz = (int)floor(Te - 0.5 * B - 0.5) + 1 + K - 1;
+    const int origin = Ra & ~3;
+    e.A = (float)(Ts - (double)origin);
+    e.B = (float)B;
+    e.E = (float)(0.5 * B);
+    e.a0 = fma_(f.a1, (float)izs, f.a0);
+    e.pad[1] = origin;
+  } else {
+    Ra = first_row(sub_(fma_(f.B, (float)izs, f.A), f.E));
+    Rz = first_row(sub_(fma_(f.B, (float)ize, f.A), f.E)) + K - 1;
+    e.pad[1] = 0;
+  }
   const int ra4 = Ra & ~3;
   const int n4 = ((Rz | 3) - ra4 + 1) >> 2;
   const bool fast = e.ncol > 0 && e.ncol <= BK_NCF && f.cl + 3 <= gp.nc - 1 && K <= 4 && Ra >= 0 &&
@@ -145,9 +169,9 @@ __device__ __forceinline__ void fill_entry(BkEntry& e, const SubFoot& f, const G
 // footprint width.  Same operations, in the same order, as the table path.
 __device__ __noinline__ float back_voxel_direct(float acc, float amp, float lo, float hi,
                                                 const BkEntry& e, const Trap& wide, int K,
-                                                const float* __restrict__ yv, int nr) {
-  const float fl = row_floor(lo);  // r0 - 1
-  const int r0 = (int)fl + 1;
+                                                const float* __restrict__ yv, int nr, int origin) {
+  const float fl = row_floor(lo);  // r0 - 1 (rows relative to origin)
+  const int r0 = (int)fl + 1 + origin;
   float g = clampf_(add_(fl, 0.5f), lo, hi);
   for (int k = 0; k < K; ++k) {
     const int r = r0 + k;
@@ -319,18 +343,21 @@ __device__ __noinline__ bool back_setup(const GridParams& gp, const ViewCoef* __
 // 3D back kernel variant of back_setup: only the first sub-footprint is kept
 // (its mask in pad[0]); the second one of a split voxel is rebuilt in the
 // view loop when needed, which halves the entry table (more L1 for y rows)
-__device__ __noinline__ bool back_setup1(const GridParams& gp, const ViewCoef* __restrict__ vcoef, int vb,
-                                         int ix, int iy, int izs, int ize, BkEntry* e) {
+__device__ __noinline__ bool back_setup1(const GridParams& gp, const ViewCoef* __restrict__ vcoef,
+                                         const ViewAx* __restrict__ vax, int vb, int ix, int iy, int izs, int ize,
+                                         BkEntry* e) {
   const int v = vb + (threadIdx.x & 31);
   BkEntry e0;
   e0.ncol = 0;
   e0.pk = 0;
+  e0.pad[1] = 0;
   int mask = 0;
   if (v < gp.nv) {
     const ViewCoef vc = vcoef[v];
     SubFoot f0, f1;
-    mask = column_footprint(vc, gp, ix, iy, f0, f1);
-    if (mask & 1) fill_entry(e0, f0, gp, izs, ize);
+    float2 c0, c1;
+    mask = column_subs(vc, gp, ix, iy, f0, f1, c0, c1) & 3;
+    if (mask & 1) fill_entry(e0, f0, gp, izs, ize, vax + v, c0);
   }
   e0.pad[0] = mask;
   *e = e0;
@@ -338,8 +365,8 @@ __device__ __noinline__ bool back_setup1(const GridParams& gp, const ViewCoef* _
 }
 
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
-    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ yT,
-    float* __restrict__ out, int accumulate) {
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
+    const float* __restrict__ yT, float* __restrict__ out, int accumulate) {
   extern __shared__ __align__(16) unsigned char bk_smem_raw[];
   BkSmem& SM = *reinterpret_cast<BkSmem*>(bk_smem_raw);
   auto& ents = SM.ents;
@@ -358,10 +385,11 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   float* qw = qbuf[warp];
   BkEntry(&my)[32] = ents[warp];
   BkEntry& sp = SM.split[warp];
-  // this lane's slices: izs + lane + 32 m, m < nvalid
+  // this lane's slices: izs + lane + 32 m, m < nvalid; entries count slices
+  // from izs and rows from a per-entry origin (fill_entry)
   const int span = ize - izs - lane;  // may be negative when nz < 32
   const int nvalid = span < 0 ? 0 : min(BK_ZPL, span / 32 + 1);
-  const float izf0 = (float)(izs + lane);
+  const float izf0 = (float)lane;
   float acc[BK_ZPL];
 #pragma unroll
   for (int m = 0; m < BK_ZPL; ++m) acc[m] = 0.0f;
@@ -369,7 +397,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   for (int vb = 0; vb < gp.nv; vb += 32) {
     // ---- lane-parallel footprint setup: lane l <- view vb + l
     // nsub = 2 when any view of this batch splits the voxel (_sf_subdivide), else 1
-    const int nsub = back_setup1(gp, vcoef, vb, ix, iy, izs, ize, &my[lane]) ? 2 : 1;
+    const int nsub = back_setup1(gp, vcoef, vax, vb, ix, iy, izs, ize, &my[lane]) ? 2 : 1;
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
     const float* yview = yb + (size_t)vb * view_elems;  // [c][r] of view vb + j
@@ -381,8 +409,9 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
           __syncwarp();  // every lane is done with the previous split entry
           if (lane == 0) {
             SubFoot f0, f1;
-            column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
-            fill_entry(sp, f1, gp, izs, ize);
+            float2 c0, c1;
+            column_subs(vcoef[vb + j], gp, ix, iy, f0, f1, c0, c1);
+            fill_entry(sp, f1, gp, izs, ize, vax + vb + j, c1);
           }
           __syncwarp();
         }
@@ -400,19 +429,22 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
             default: row_sums<4>(q4, yv, nr, ef.ts, n4, lane); break;
           }
           __syncwarp();
-          const int K = (pk >> 1) & 7, ra4 = pk >> 16;
+          // the table starts at the entry's row origin (ra4): relative row 0
+          const int K = (pk >> 1) & 7;
           const BkEntry e = ef;
-          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, ra4);
-          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, ra4);
-          else back_slices<4>(acc, e, izf0, nvalid, qw, ra4);
+          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, 0);
+          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, 0);
+          else back_slices<4>(acc, e, izf0, nvalid, qw, 0);
           __syncwarp();
           continue;
         }
         if (ef.ncol == 0) continue;
         const BkEntry& e = ef;  // (shared memory: no private copy on the rare paths)
         const int K = rows_per_slice(e.B);
-        const int Ra = first_row(sub_(fma_(e.B, (float)izs, e.A), e.E));
-        const int Rz = first_row(sub_(fma_(e.B, (float)ize, e.A), e.E)) + K - 1;
+        const int origin = e.pad[1];
+        const int Rar = first_row(sub_(e.A, e.E));  // relative to origin
+        const int Ra = Rar + origin;
+        const int Rz = first_row(sub_(fma_(e.B, (float)(ize - izs), e.A), e.E)) + K - 1 + origin;
         if (Rz < 0 || Ra > nr - 1) continue;
         const float* yv = yview;  // [c][r] of the view
         const int nq = Rz - Ra + 1;
@@ -456,9 +488,9 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
             }
           }
           __syncwarp();
-          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Ra);
-          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, Ra);
-          else back_slices<4>(acc, e, izf0, nvalid, qw, Ra);
+          if (K == 2) back_slices<2>(acc, e, izf0, nvalid, qw, Rar);
+          else if (K == 3) back_slices<3>(acc, e, izf0, nvalid, qw, Rar);
+          else back_slices<4>(acc, e, izf0, nvalid, qw, Rar);
           __syncwarp();
         } else {
           Trap wide{};
@@ -475,7 +507,7 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
             const float lo = sub_(T, e.E), hi = add_(T, e.E);
             const float q = fma_(e.a1, izf, e.a0);
             const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
-            acc[m] = back_voxel_direct(acc[m], amp, lo, hi, e, wide, K, yv, nr);
+            acc[m] = back_voxel_direct(acc[m], amp, lo, hi, e, wide, K, yv, nr, origin);
           }
         }
       }
@@ -570,6 +602,24 @@ __device__ __forceinline__ void write_entry(FwEntry& e, const SubFoot& f, int co
   e.za4 = 0;
   e.nst = 0;
   e.info = 0;
+}
+
+// 3D forward: replace the entry's f32 absolute axial map by the f64 one at
+// the (sub-)voxel centre, RELATIVE to the band's first row rw0 (the kernel
+// then counts rows from rw0), so fp32 resolves footprint edges to ~1e-5 row
+// on 1536-row detectors (round 1: absolute rows, 1.2e-4 row at C5).
+__device__ __forceinline__ void localize_entry(FwEntry& e, const ViewAx& ax, const GridParams& gp, float2 cxy,
+                                               int rw0) {
+  double A, B;
+  axial64(ax, gp.kind, (double)cxy.x, (double)cxy.y, A, B);
+  // A, B, E decide the footprint edges (f64 -> f32 relative to rw0); invB and
+  // cb only bound the candidate slices (0.01-slice margins): fp32 suffices
+  const double Ar = A - (double)rw0;
+  e.A = (float)Ar;
+  e.B = (float)B;
+  e.E = (float)(0.5 * B);
+  e.invB = __frcp_rn(e.B);
+  e.cb = (-0.5f - e.E - e.A) * e.invB - 0.01f;
 }
 
 // Band-specific part of an entry, evaluated by the lane that set the entry up:
@@ -857,7 +907,7 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
                                            const GridParams& gp, const float* __restrict__ xb,
                                            int rw0, int lane) {
   float* xs = S.xs;
-  const float rbase = (float)fw_row_base(rw0, lane);
+  const float rbase = (float)fw_row_base(rw0, lane);  // rw0 = 0: rows relative to the band
   // software pipeline: x of the next fast-path entry is in flight while the
   // current entry is gathered
   constexpr bool ASYNC = VEC && CTP_FW_CPASYNC;
@@ -962,12 +1012,12 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
         xs[FW_XPAD + i] = mul_(amp, __ldg(xc + piece + i));
       }
       __syncwarp();
-#pragma unroll
 #if CTP_FW_PAIRS
       const int k0 = g0 & ~1, k1 = g1 | 1;
 #else
       const int k0 = g0, k1 = g1;
 #endif
+#pragma unroll
       for (int kk = 0; kk < FW_KR; ++kk) {
         if (kk < k0 || kk > k1) continue;
         const float rf = fw_row_of(rbase, kk);
@@ -997,9 +1047,10 @@ __device__ __forceinline__ void fw_process(FvSmem& S, int nent, float (&acc)[FW_
 // (sub-)footprints into ent[0..).  Returns how many entries the warp added.
 // Out of line: it holds most of the kernel's geometry, and keeping it out of
 // the gather loop's register allocation avoids rematerialisation there.
-__device__ __noinline__ int fw_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp, FwEntry* ent,
-                                          int k, int total, int ib, int excl, int jl, bool primary_x, int c0,
-                                          int cw, float band_lo, float band_hi, int rw0, int rw1, bool vec) {
+__device__ __noinline__ int fw_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp,
+                                          const ViewAx* __restrict__ vaxp, FwEntry* ent, int k, int total, int ib,
+                                          int excl, int jl, bool primary_x, int c0, int cw, float band_lo,
+                                          float band_hi, int rw0, int rw1, bool vec) {
   const int lane = threadIdx.x & 31;
   // owner lane o: the largest lane with excl_o <= k (it has cnt_o > 0)
   int o = 0;
@@ -1011,13 +1062,14 @@ __device__ __noinline__ int fw_candidates(const GridParams& gp, const ViewCoef* 
   const int jo = __shfl_sync(0xffffffffu, jl, o);
   const int exo = __shfl_sync(0xffffffffu, excl, o);
   SubFoot f0, f1;
+  float2 cxy0 = make_float2(0.0f, 0.0f), cxy1 = cxy0;
   int mask = 0, col = 0;
   if (k < total) {
     const ViewCoef vc = *vcp;
     const int ii = ib + o, j = jo + (k - exo);
     const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
     col = iy * gp.nx + ix;
-    mask = column_footprint(vc, gp, ix, iy, f0, f1);
+    mask = column_subs(vc, gp, ix, iy, f0, f1, cxy0, cxy1) & 3;
     if ((mask & 1) && !reaches_tile(f0, gp, c0, cw, band_lo, band_hi)) mask &= ~1;
     if ((mask & 2) && !reaches_tile(f1, gp, c0, cw, band_lo, band_hi)) mask &= ~2;
   }
@@ -1026,19 +1078,21 @@ __device__ __noinline__ int fw_candidates(const GridParams& gp, const ViewCoef* 
   const int off = ni - n;
   if (mask & 1) {
     write_entry(ent[off], f0, col, c0, cw);
-    band_info(ent[off], gp, rw0, rw1, vec);
+    localize_entry(ent[off], *vaxp, gp, cxy0, rw0);
+    band_info(ent[off], gp, 0, rw1 - rw0, vec);
   }
   if (mask & 2) {
     write_entry(ent[off + (mask & 1)], f1, col, c0, cw);
-    band_info(ent[off + (mask & 1)], gp, rw0, rw1, vec);
+    localize_entry(ent[off + (mask & 1)], *vaxp, gp, cxy1, rw0);
+    band_info(ent[off + (mask & 1)], gp, 0, rw1 - rw0, vec);
   }
   return __shfl_sync(0xffffffffu, ni, 31);
 }
 
 template <bool VEC>
 __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
-    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xT,
-    float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
+    const float* __restrict__ xT, float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FvSmem& S = reinterpret_cast<FvSmem*>(smem_raw)[warp];
@@ -1120,17 +1174,17 @@ __global__ void __launch_bounds__(FV_WARPS * 32, CTP_FW_MINB) sf_forward_kernel(
     const int excl = incl - cnt;
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
-      pending += fw_candidates(gp, vcoef + v, S.ent + pending, cbase + lane, total, ib, excl, jl, primary_x,
+      pending += fw_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl, primary_x,
                                c0, cw, band_lo, band_hi, rw0, rw1, VEC);
       __syncwarp();
       if (pending >= 32) {
-        fw_process<VEC>(S, pending, acc, gp, xb, rw0, lane);
+        fw_process<VEC>(S, pending, acc, gp, xb, 0, lane);
         pending = 0;
         __syncwarp();
       }
     }
   }
-  if (pending > 0) fw_process<VEC>(S, pending, acc, gp, xb, rw0, lane);
+  if (pending > 0) fw_process<VEC>(S, pending, acc, gp, xb, 0, lane);
 
   // store the tile: y[b][v][r][c0 + c]
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
@@ -1480,14 +1534,19 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
   const dim3 block(256);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = min(65535, batch - b0);
-    const dim3 grid((C + 31) / 32, (R + 31) / 32, nb);
-    transpose_kernel<<<grid, block, 0, st>>>(in, out, R, C, b0);
+    // row blocks in launches of <= 65535 (gridDim.y limit): large fan sinograms
+    // and slices (nv*nc or nx*ny above ~2.1M elements) need several
+    const int nrb = (R + 31) / 32;
+    for (int rb0 = 0; rb0 < nrb; rb0 += 65535) {
+      const dim3 grid((C + 31) / 32, min(65535, nrb - rb0), nb);
+      transpose_kernel<<<grid, block, 0, st>>>(in, out, R, C, b0, rb0);
+    }
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
-                        int batch, bool accumulate, cudaStream_t st) {
+cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
+                        float* vol, int batch, bool accumulate, cudaStream_t st) {
   cudaError_t ea = cudaFuncSetAttribute(sf_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BkSmem));
   if (ea != cudaSuccess) return ea;
@@ -1497,14 +1556,14 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float
     const dim3 grid(nbx * nby, (gp.nz + BK_ZC - 1) / BK_ZC, nb);
     const size_t sino_elems = (size_t)gp.nv * gp.nr * gp.nc;
     const size_t vol_elems = (size_t)gp.nx * gp.ny * gp.nz;
-    sf_back_kernel<<<grid, BK_WARPS * 32, sizeof(BkSmem), st>>>(gp, vcoef, yT + (size_t)b0 * sino_elems,
+    sf_back_kernel<<<grid, BK_WARPS * 32, sizeof(BkSmem), st>>>(gp, vcoef, vax, yT + (size_t)b0 * sino_elems,
                                                                 vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const float* xT, float* sino,
-                           int batch, bool accumulate, cudaStream_t st) {
+cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                           float* sino, int batch, bool accumulate, cudaStream_t st) {
   const size_t smem = forward_warp_smem_bytes();
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
@@ -1523,7 +1582,7 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const fl
     const long long rem = ntasks - t0;
     const long long nb = (rem + FV_WARPS - 1) / FV_WARPS;
     const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
-    kern<<<grid, FV_WARPS * 32, smem, st>>>(g2, vcoef, xT, sino, accumulate ? 1 : 0, t0, ntasks);
+    kern<<<grid, FV_WARPS * 32, smem, st>>>(g2, vcoef, vax, xT, sino, accumulate ? 1 : 0, t0, ntasks);
   }
   return cudaGetLastError();
 }

@@ -12,12 +12,13 @@ namespace ctp {
 
 cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batch,
                              cudaStream_t st);
-// xT: volume in [batch][ny*nx][nz] layout; sino: [batch][nv][nr][nc]
-cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const float* xT,
+// 3D pair.  xT: volume in [batch][ny*nx][nz] layout;
+// sino: [batch][nv][nr][nc]
+cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
                            float* sino, int batch, bool accumulate, cudaStream_t st);
 // yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]
-cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const float* yT, float* vol,
-                        int batch, bool accumulate, cudaStream_t st);
+cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
+                        float* vol, int batch, bool accumulate, cudaStream_t st);
 size_t forward_warp_smem_bytes();
 // fan beam (nz == nr == 1) with the batch innermost: xB [ny*nx][batch], yB [nv][nc][batch]
 cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,

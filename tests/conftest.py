@@ -72,3 +72,5 @@ def max_abs_rel(a, b):
 REL_L2_TOL = 1e-4
 MAX_ABS_TOL = 1e-4
 ADJOINT_TOL = 1e-5
+#: explicit-matrix transpose bound of the 3D pair, relative to max|A| (fp32 rounding)
+TRANSPOSE_TOL = 4e-6
