@@ -12,10 +12,15 @@ forward+backward of ``Projector`` costs).
 
     GUPS = 2 * nx*ny*nz * nv / t_step / 1e9     (voxel-view updates per second)
 
-N > 1 (torchrun, one process per GPU): views sharded over ranks; forward has
-no communication, back ends with an NCCL reduce-scatter of the partial
-volumes (paper_2307_05801_b200/partition.py).  Total work is fixed, so
-"scaling" is "strong"; time = max over ranks.
+N > 1: one process per GPU.  Without a torchrun environment, ``--gpus N``
+re-launches itself under ``python -m torch.distributed.run --nproc-per-node N``
+(127.0.0.1, a free port, NCCL_DEBUG=INFO so the N-rank communicator shows in
+the log); with one it checks WORLD_SIZE == N.  Views are sharded over ranks;
+the forward has no communication, the back projection is fused with per-z-
+chunk NCCL reductions to the z-slab owners (csrc/dist.cu, overlapped with the
+remaining back projection).  Total work is fixed, so "scaling" is "strong";
+time = max over ranks; per-rank times and the exposed reduction time are
+reported under "dist".
 
 Inputs (512 MiB volume, 1.58 GiB sinogram) exceed the 126 MB L2, so no L2
 flush is needed between timed iterations.  ``--impl reference`` times the
@@ -220,6 +225,34 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def _spawn_or_check(args):
+    """--gpus N > 1 outside torchrun: re-run this command under torchrun with N
+    local ranks; inside torchrun: WORLD_SIZE must equal N."""
+    if args.impl == "reference":
+        return  # rank 0 alone runs the host baseline; no ranks needed
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        import socket
+        import subprocess
+
+        import torch
+
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {n} CUDA device(s) visible"}), flush=True)
+            raise SystemExit(2)
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd, env=env))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with --nproc-per-node {args.gpus}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -234,6 +267,7 @@ def main():
     ap.add_argument("--views", type=int, default=0,
                     help="profiling only: restrict to the first N views (not a bench number)")
     args = ap.parse_args()
+    _spawn_or_check(args)
     cfg = dict(CONFIGS[args.config])
     if args.views:
         cfg["numAngles"] = args.views
@@ -270,19 +304,16 @@ def main():
     plan = sharded.shard.plan(local)
     sino_out = torch.empty((B, nv_local, nr, nc), device=dev)
 
+    slab_out = None
+    if world > 1:
+        slab_out = torch.empty((B, sharded.slab) + spec.shape[1:], device=dev)
+
     def step(time_kernel=False):
         plan.forward(x, out=sino_out, time_kernel=time_kernel)
         if world == 1:
-            vol = plan.back(y, time_kernel=time_kernel)
-        else:
-            vol = sharded.back(y) if B > 1 else None
-            if B == 1:
-                part = torch.zeros((1, sharded.nz_pad) + spec.shape[1:], device=dev)
-                plan.back(y, out=part[:, : spec.numZ], time_kernel=time_kernel)
-                out = torch.empty((sharded.slab,) + spec.shape[1:], device=dev)
-                dist.reduce_scatter_tensor(out, part[0])
-                vol = out
-        return vol
+            return plan.back(y, time_kernel=time_kernel)
+        # fused back projection + per-z-chunk NCCL reductions (csrc/dist.cu)
+        return sharded.back_native(y, out=slab_out)
 
     for _ in range(args.warmup):
         step()
@@ -299,20 +330,46 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            step(time_kernel=True)
+        eb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for i in range(args.steps):
+            plan.forward(x, out=sino_out, time_kernel=True)
+            eb[i][0].record(stream)
+            if world == 1:
+                plan.back(y, time_kernel=True)
+            else:
+                sharded.back_native(y, out=slab_out)
+            eb[i][1].record(stream)
             fwd_ms.append(plan.kernel_time_ms(0))
-            back_ms.append(plan.kernel_time_ms(1))
+            if world == 1:
+                back_ms.append(plan.kernel_time_ms(1))
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     t_ms = e0.elapsed_time(e1)
     t_max = t_ms
+    dist_info = None
     if world > 1:
         tt = torch.tensor([t_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
+        fused_ms = statistics.mean(a.elapsed_time(b) for a, b in eb)
+        # the same back projection without the reductions (untimed): what the
+        # fused call's communication adds on the critical path
+        part = torch.empty((B,) + spec.shape, device=dev)
+        for _ in range(args.steps):
+            plan.back(y, out=part, time_kernel=True)
+            back_ms.append(plan.kernel_time_ms(1))
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, {"rank": rank, "step_ms": t_ms / args.steps, "views": [a, b],
+                                          "fwd_kernel_ms": statistics.mean(fwd_ms),
+                                          "back_fused_ms": fused_ms,
+                                          "back_kernel_ms": statistics.mean(back_ms)})
+        dist_info = {"ranks": per_rank,
+                     "reduce_exposed_ms": max(r["back_fused_ms"] - r["back_kernel_ms"] for r in per_rank),
+                     "reduce_bytes_per_rank": 4 * B * nvox,
+                     "collective": "ncclReduce per (z-chunk of 256 slices, owner), grouped, on a comm stream"}
     total_updates = 2.0 * B * nvox * g.numViews * args.steps
     value = total_updates / (t_max / 1e3) / 1e9
 
@@ -403,8 +460,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 4 * args.steps if world == 1 else (2 + 1 + -(-spec.numZ // 256)) * args.steps,
         }
+        if dist_info is not None:
+            line["dist"] = dist_info
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -159,6 +159,43 @@ int ctp_sf_forward_oneshot(const ctp_geom* geom, const float* vol, float* sino,
 int ctp_sf_back_oneshot(const ctp_geom* geom, const float* sino, float* vol,
                         int batch, void* stream);
 
+/* ---- multi-GPU (north_star item 4; the reference has no multi-device path) ----
+ *
+ * One process per GPU.  Views are sharded over ranks: rank r holds a plan over
+ * its contiguous view range [a_r, b_r) and the FULL grid.  The forward needs no
+ * communication (ctp_sf_forward on the shard writes the rank's views).  The
+ * back projection of the shard is fused with the reduction across ranks:
+ *
+ *   ctp_sf_back_sharded: x_r = sum over ranks of A_shard^T y_shard, restricted
+ *   to rank r's z-slab [r*S, (r+1)*S), S = ceil(nz / nranks) (slices past nz
+ *   are zero).  The partial volume is produced in z-chunks of
+ *   CTP_BACK_ZCHUNK slices on `stream`; as soon as a chunk is done, its parts
+ *   are ncclReduce'd (sum, fp32) to the ranks owning them on the
+ *   communicator's own stream, overlapped with the next chunk's back
+ *   projection.  Equivalent to one reduce-scatter of the whole partial volume.
+ *   `stream` waits for the last reduction: stream-ordered, no host sync.
+ *
+ * NCCL is loaded at run time (dlopen of libnccl.so.2, reusing the copy torch
+ * already loaded); the library has no link-time NCCL dependency.
+ */
+#define CTP_BACK_ZCHUNK 256
+
+typedef struct ctp_dist ctp_dist;
+
+/* Fills id (128 bytes, an ncclUniqueId) on the root rank; share the bytes
+ * with the other ranks out of band (e.g. torch.distributed). */
+int ctp_dist_unique_id(unsigned char* id, size_t id_bytes);
+/* Communicator of `nranks` processes, this one being `rank`, on `device`. */
+int ctp_dist_create(const unsigned char* id, size_t id_bytes, int nranks, int rank, int device,
+                    ctp_dist** out);
+int ctp_dist_destroy(ctp_dist* dist);
+/* Slab owned by `rank`: first slice and slice count S (slices >= nz are padding). */
+int ctp_dist_slab(const ctp_plan* plan, const ctp_dist* dist, int rank, int* z_first, int* z_count);
+size_t ctp_sf_back_sharded_workspace_bytes(const ctp_plan* plan, const ctp_dist* dist, int batch);
+/* sino: this rank's views [batch][nv_r][nr][nc]; slab: [batch][S][ny][nx]. */
+int ctp_sf_back_sharded(const ctp_plan* plan, ctp_dist* dist, const float* sino, float* slab, int batch,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

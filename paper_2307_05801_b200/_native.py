@@ -60,6 +60,12 @@ EXPORTED_SYMBOLS = (
     "ctp_sf_back_oneshot",
     "ctp_siddon_forward",
     "ctp_siddon_back",
+    "ctp_dist_unique_id",
+    "ctp_dist_create",
+    "ctp_dist_destroy",
+    "ctp_dist_slab",
+    "ctp_sf_back_sharded_workspace_bytes",
+    "ctp_sf_back_sharded",
 )
 
 
@@ -138,6 +144,18 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = [vp, ctypes.c_double, vp, vp, i32, u32, vp]
             fn.restype = i32
+        lib.ctp_dist_unique_id.argtypes = [ctypes.c_char_p, sz]
+        lib.ctp_dist_unique_id.restype = i32
+        lib.ctp_dist_create.argtypes = [ctypes.c_char_p, sz, i32, i32, i32, ctypes.POINTER(vp)]
+        lib.ctp_dist_create.restype = i32
+        lib.ctp_dist_destroy.argtypes = [vp]
+        lib.ctp_dist_destroy.restype = i32
+        lib.ctp_dist_slab.argtypes = [vp, vp, i32, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        lib.ctp_dist_slab.restype = i32
+        lib.ctp_sf_back_sharded_workspace_bytes.argtypes = [vp, vp, i32]
+        lib.ctp_sf_back_sharded_workspace_bytes.restype = sz
+        lib.ctp_sf_back_sharded.argtypes = [vp, vp, vp, vp, i32, vp, sz, vp]
+        lib.ctp_sf_back_sharded.restype = i32
         if lib.ctp_abi_version() != ABI_VERSION:
             raise NativeLibraryError(
                 f"ABI version mismatch: library {lib.ctp_abi_version()} != binding {ABI_VERSION}")
@@ -200,9 +218,16 @@ class Plan:
             _raise_status(self.lib, st, "ctp_plan_kernel_time_ms")
         return float(ms.value)
 
+    def _check_io(self, direction: int, inp, out):
+        in_shape = self.vol_shape if direction == 0 else self.sino_shape
+        out_shape = self.sino_shape if direction == 0 else self.vol_shape
+        _check_device_tensor(inp, (None,) + tuple(in_shape), self.device, "input")
+        _check_device_tensor(out, (int(inp.shape[0]),) + tuple(out_shape), self.device, "output")
+
     def _run(self, direction: int, inp, out, accumulate: bool, time_kernel: bool = False):
         import torch
 
+        self._check_io(direction, inp, out)
         batch = int(inp.shape[0])
         nbytes = self.workspace_bytes(direction, batch)
         ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -219,6 +244,7 @@ class Plan:
 
         # kernel_geom's parallel-beam ray back-off (_common.py:21-24), same expression
         back = float(self.spec.circumscribed_radius() + self.spec.voxelWidth)
+        self._check_io(direction, inp, out)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         fn = self.lib.ctp_siddon_forward if direction == 0 else self.lib.ctp_siddon_back
         flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_TIME_KERNEL if time_kernel else 0)
@@ -260,9 +286,100 @@ class Plan:
         return self._run(1, y, out, accumulate, time_kernel)
 
 
+class Dist:
+    """A ctp_dist: NCCL communicator of the view-sharded back projection
+    (include/ctproj_b200.h, multi-GPU section).  ``unique_id`` (128 bytes) is
+    made by ``Dist.make_id()`` on rank 0 and shared out of band."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def make_id() -> bytes:
+        lib = load_library()
+        buf = ctypes.create_string_buffer(Dist.ID_BYTES)
+        st = lib.ctp_dist_unique_id(buf, Dist.ID_BYTES)
+        if st != CTP_OK:
+            _raise_status(lib, st, "ctp_dist_unique_id")
+        return buf.raw
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, device_index: int):
+        self.lib = load_library()
+        if len(unique_id) != self.ID_BYTES:
+            raise InvalidValueError("unique_id must be 128 bytes")
+        h = ctypes.c_void_p()
+        st = self.lib.ctp_dist_create(unique_id, self.ID_BYTES, int(nranks), int(rank), int(device_index),
+                                      ctypes.byref(h))
+        if st != CTP_OK:
+            _raise_status(self.lib, st, "ctp_dist_create")
+        self._h = h
+        self.nranks, self.rank, self.device_index = int(nranks), int(rank), int(device_index)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self.lib.ctp_dist_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def slab(self, plan: "Plan", rank: int | None = None):
+        """(first slice, slice count) of ``rank``'s z-slab (default: this rank)."""
+        z0, n = ctypes.c_int(), ctypes.c_int()
+        st = self.lib.ctp_dist_slab(plan._h, self._h, self.rank if rank is None else int(rank),
+                                    ctypes.byref(z0), ctypes.byref(n))
+        if st != CTP_OK:
+            _raise_status(self.lib, st, "ctp_dist_slab")
+        return z0.value, n.value
+
+    def back_sharded(self, plan: "Plan", y, out=None):
+        """This rank's z-slab [B, S, ny, nx] of sum_ranks A_shard^T y_shard:
+        back projection of ``y`` ([B, nv_r, nr, nc], this rank's views, on the
+        plan's device) fused with per-z-chunk NCCL reductions to the slab
+        owners, overlapped with the remaining back projection."""
+        import torch
+
+        _check_device_tensor(y, (None,) + plan.sino_shape, plan.device, "y")
+        B = int(y.shape[0])
+        _, S = self.slab(plan)
+        spec = plan.spec
+        if out is None:
+            out = torch.empty((B, S, spec.numY, spec.numX), dtype=torch.float32, device=plan.device)
+        _check_device_tensor(out, (B, S, spec.numY, spec.numX), plan.device, "out")
+        nbytes = int(self.lib.ctp_sf_back_sharded_workspace_bytes(plan._h, self._h, B))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=plan.device)
+        stream = torch.cuda.current_stream(plan.device).cuda_stream
+        st = self.lib.ctp_sf_back_sharded(plan._h, self._h, y.data_ptr(), out.data_ptr(), B, ws.data_ptr(),
+                                          nbytes, stream)
+        if st != CTP_OK:
+            _raise_status(self.lib, st, "ctp_sf_back_sharded")
+        return out
+
+
+def _check_device_tensor(t, shape, device, what):
+    """f32, contiguous, on ``device``, matching ``shape`` (None = any extent):
+    anything else would be read out of bounds by the kernels."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidValueError(f"{what} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise InvalidValueError(f"{what} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise InvalidValueError(f"{what} must be contiguous")
+    if t.device != device:
+        raise InvalidValueError(f"{what} is on {t.device}, the plan on {device}")
+    if len(t.shape) != len(shape) or any(s is not None and int(a) != int(s) for a, s in zip(t.shape, shape)):
+        raise SpecMismatchError(f"{what} has shape {tuple(t.shape)}, expected "
+                                f"{tuple('B' if s is None else s for s in shape)}")
+
+
 _plans: "OrderedDict[tuple, Plan]" = OrderedDict()
 _plans_lock = threading.Lock()
-_PLAN_CACHE_SIZE = 16
+_PLAN_CACHE_SIZE = 64  # z-slab streaming builds one plan per slab (ADVICE r1)
 
 
 def get_plan(g: Geometry, spec: VolumeSpec, device_index: int) -> Plan:

@@ -22,22 +22,9 @@ using ctp::GridParams;
 using ctp::ViewAx;
 using ctp::ViewCoef;
 
-struct ctp_plan {
-  ctp_geom geom;               // scalars (poses pointer cleared)
-  std::vector<double> poses;   // host copy, nv*15
-  int device;
-  ViewCoef* d_coef;            // device, nv entries
-  ViewAx* d_ax;                // device, nv entries (f64 axial map of the 3D kernels)
-  double* d_pose;              // device, nv*15 float64 (Siddon pair)
-  bool sf_ok;                  // SF supports this geometry (SF-modular: upright panels only)
-  std::string sf_reason;
-  GridParams gp;
-  size_t vol_elems, sino_elems;
-  cudaEvent_t ev[2][2];        // [direction][start/stop], created lazily
-  bool ev_recorded[2];
-};
+#include "plan_internal.h"
 
-namespace {
+namespace ctp_internal {
 
 thread_local std::string g_last_error;
 
@@ -51,21 +38,14 @@ int cuda_fail(cudaError_t e, const char* where) {
   return e == cudaErrorMemoryAllocation ? CTP_ERR_OUT_OF_MEMORY : CTP_ERR_CUDA;
 }
 
-struct DeviceGuard {
-  int prev = -1;
-  bool switched = false;
-  cudaError_t err = cudaSuccess;
-  explicit DeviceGuard(int dev) {
-    err = cudaGetDevice(&prev);
-    if (err == cudaSuccess && dev >= 0 && dev != prev) {
-      err = cudaSetDevice(dev);
-      switched = (err == cudaSuccess);
-    }
-  }
-  ~DeviceGuard() {
-    if (switched) cudaSetDevice(prev);
-  }
-};
+}  // namespace ctp_internal
+
+using ctp_internal::DeviceGuard;
+using ctp_internal::cuda_fail;
+using ctp_internal::fail;
+using ctp_internal::g_last_error;
+
+namespace {
 
 int validate(const ctp_geom* g) {
   if (!g) return fail(CTP_ERR_INVALID_ARGUMENT, "geometry pointer is null");

@@ -94,6 +94,7 @@ constexpr int BK_ZPL = CTP_BK_ZPL;      // voxels per lane
 constexpr int BK_CX = CTP_BK_CX;  // voxel columns along x per CTA (BK_WARPS / BK_CX along y)
 static_assert(BK_WARPS % BK_CX == 0, "CTAs cover BK_CX x BK_WARPS/BK_CX voxel columns");
 constexpr int BK_ZC = 32 * BK_ZPL;  // slices per warp
+static_assert(BK_ZC == kBackZBlock, "sf_launch.h advertises the z-block size");
 #ifndef CTP_BK_QMAX
 #define CTP_BK_QMAX (BK_ZC * 25 / 16)  // rows covered by slices with B <= 1.5 (+ margin)
 #endif
@@ -366,7 +367,7 @@ __device__ __noinline__ bool back_setup1(const GridParams& gp, const ViewCoef* _
 
 __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
-    const float* __restrict__ yT, float* __restrict__ out, int accumulate) {
+    const float* __restrict__ yT, float* __restrict__ out, int accumulate, int z0, int z1) {
   extern __shared__ __align__(16) unsigned char bk_smem_raw[];
   BkSmem& SM = *reinterpret_cast<BkSmem*>(bk_smem_raw);
   auto& ents = SM.ents;
@@ -377,8 +378,8 @@ __global__ void __launch_bounds__(BK_WARPS * 32, CTP_BK_MINB) sf_back_kernel(
   const int iy = (blockIdx.x / nbx) * (BK_WARPS / BK_CX) + (warp / BK_CX);
   if (ix >= gp.nx || iy >= gp.ny) return;  // warp-uniform; no CTA barriers below
   const int b = blockIdx.z;
-  const int izs = blockIdx.y * BK_ZC;
-  const int ize = min(izs + BK_ZC, gp.nz) - 1;
+  const int izs = z0 + blockIdx.y * BK_ZC;  // slices [z0, z1) of this launch
+  const int ize = min(izs + BK_ZC, z1) - 1;
   const int nr = gp.nr, nc = gp.nc;
   const size_t view_elems = (size_t)nc * nr;
   const float* yb = yT + (size_t)b * gp.nv * view_elems;
@@ -1546,18 +1547,21 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 }
 
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
-                        float* vol, int batch, bool accumulate, cudaStream_t st) {
+                        float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
+  if (z1 < 0) z1 = gp.nz;
+  if (z0 < 0 || z0 >= z1 || z1 > gp.nz) return cudaErrorInvalidValue;
   cudaError_t ea = cudaFuncSetAttribute(sf_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BkSmem));
   if (ea != cudaSuccess) return ea;
   const int nbx = (gp.nx + BK_CX - 1) / BK_CX, nby = (gp.ny + BK_WARPS / BK_CX - 1) / (BK_WARPS / BK_CX);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = min(65535, batch - b0);
-    const dim3 grid(nbx * nby, (gp.nz + BK_ZC - 1) / BK_ZC, nb);
+    const dim3 grid(nbx * nby, (z1 - z0 + BK_ZC - 1) / BK_ZC, nb);
     const size_t sino_elems = (size_t)gp.nv * gp.nr * gp.nc;
     const size_t vol_elems = (size_t)gp.nx * gp.ny * gp.nz;
     sf_back_kernel<<<grid, BK_WARPS * 32, sizeof(BkSmem), st>>>(gp, vcoef, vax, yT + (size_t)b0 * sino_elems,
-                                                                vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0);
+                                                                vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0,
+                                                                z0, z1);
   }
   return cudaGetLastError();
 }

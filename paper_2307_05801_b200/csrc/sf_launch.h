@@ -16,9 +16,11 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 // sino: [batch][nv][nr][nc]
 cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
                            float* sino, int batch, bool accumulate, cudaStream_t st);
-// yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]
+// yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]; only
+// slices [z0, z1) of vol are written (z1 < 0: nz)
+constexpr int kBackZBlock = 256;  // slices per back-kernel z-block (BK_ZC)
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
-                        float* vol, int batch, bool accumulate, cudaStream_t st);
+                        float* vol, int batch, bool accumulate, cudaStream_t st, int z0 = 0, int z1 = -1);
 size_t forward_warp_smem_bytes();
 // fan beam (nz == nr == 1) with the batch innermost: xB [ny*nx][batch], yB [nv][nc][batch]
 cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,

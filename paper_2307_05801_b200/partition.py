@@ -6,10 +6,15 @@ section 0, gap 3); this module adds it around the unchanged single-GPU pair:
 
 * forward: rank r projects views [a_r, b_r) of the full (replicated) volume
   -- no communication at all;
-* back:    rank r back-projects its views into a full-size partial volume,
-  then ONE reduce-scatter (sum, fp32) over NCCL / NVLink leaves each rank the
-  z-slab it owns of A^T y (``back``), or an all-reduce leaves every rank the
-  whole volume (``back_replicated``).
+* back:    rank r back-projects its views into a full-size partial volume and
+  the partial volumes are summed so that each rank owns one z-slab of A^T y
+  (``back``), or an all-reduce leaves every rank the whole volume
+  (``back_replicated``).  On NCCL process groups the SF back projection goes
+  through the native fused path (``ctp_sf_back_sharded``, csrc/dist.cu): the
+  partial volume is produced in 256-slice z-chunks and each finished chunk is
+  reduced to its slab owners on a communication stream while the next chunk
+  is back-projected.  Otherwise (gloo tests, Siddon)
+  one reduce-scatter follows the whole back projection.
 
 Parallel beam (``ZSlabParallelProjector``): rank r owns detector rows
 [r0, r1) in the forward and volume slices [z0, z1) in the back projection,
@@ -86,6 +91,34 @@ class ViewShardedProjector:
         nz = pair.volumeSpec.numZ
         self.slab = slab_size(nz, world)
         self.nz_pad = self.slab * world
+        self._dist = None
+        self.native = False
+        if isinstance(backend, CudaBackend) and pair.model == "sf" and world > 1:
+            import torch.distributed as dist
+
+            self.native = dist.is_initialized() and dist.get_backend(group) == "nccl"
+
+    def native_dist(self):
+        """The rank's ctp_dist (NCCL communicator of the fused back projection),
+        created on first use; the 128-byte id travels over the process group."""
+        if self._dist is None:
+            from ._native import Dist
+
+            if self.world == 1:
+                self._dist = Dist(Dist.make_id(), 1, 0, self.backend.device_index)
+            else:
+                import torch.distributed as dist
+
+                obj = [Dist.make_id() if self.rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=self.group)
+                self._dist = Dist(obj[0], self.world, self.rank, self.backend.device_index)
+        return self._dist
+
+    def back_native(self, y_local, out=None):
+        """Fused back projection + per-z-chunk reductions (csrc/dist.cu): this
+        rank's z-slab [B, slab, ny, nx]."""
+        plan = self.shard.plan(self.backend.device_index)
+        return self.native_dist().back_sharded(plan, y_local.contiguous(), out=out)
 
     # -- forward: no communication -------------------------------------------
     def forward(self, x):
@@ -112,6 +145,8 @@ class ViewShardedProjector:
         import torch
         import torch.distributed as dist
 
+        if self.native:
+            return self.back_native(y_local)
         part = self._partial(y_local)
         if self.world == 1:
             return part
