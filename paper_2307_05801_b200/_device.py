@@ -6,8 +6,9 @@ through the cached ``_native.Plan``:
 * CUDA tensor in  -> CUDA tensor out, on the input's device, stream-ordered
   on torch's current stream (no host synchronisation);
 * CPU tensor / numpy in -> the same type out.  Inputs are staged through
-  pinned memory and copied in view- or slice-chunks by ``Streamer``
-  (chunked H2D / compute / D2H overlap, see chunking.py).
+  pinned memory and streamed block by block (view chunks x z-slabs sized to
+  the device budget, chunked H2D / compute / D2H overlap, see chunking.py),
+  so neither the whole volume nor the whole sinogram has to fit on the GPU.
 
 There is no CPU arithmetic path: a machine without a GPU gets a
 ``NativeLibraryError`` / ``CudaRuntimeError``, never silent CPU results.
@@ -58,17 +59,14 @@ def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None, 
         with torch.cuda.device(batch.device):
             return plan.forward(x, out=out) if direction == 0 else plan.back(x, out=out)
     # host input: numpy array or CPU tensor
-    from .chunking import host_apply, zslab_apply
+    from .chunking import device_budget, plan_blocks, stream_apply
 
     plan = plan_for(g, spec)
     as_numpy = not isinstance(batch, torch.Tensor)
     host = torch.from_numpy(np.ascontiguousarray(batch, dtype=np.float32)) if as_numpy else batch
     host = host.to(torch.float32).contiguous()
-    nzs = zslab_slices(g, spec, int(host.shape[0]), plan.device)
-    if 0 < nzs < spec.numZ:
-        res = zslab_apply(plan, host, direction, nzs)
-    else:
-        res = host_apply(plan, host, direction)
+    nzs, ranges = plan_blocks(g, spec, int(host.shape[0]), device_budget(plan.device))
+    res = stream_apply(plan, host, direction, nzs, ranges)
     return res.numpy() if as_numpy else res
 
 
@@ -92,27 +90,3 @@ def _run_siddon(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None):
         res = plan.siddon_forward(xd) if direction == 0 else plan.siddon_back(xd)
         res = res.cpu()
     return res.numpy() if as_numpy else res
-
-
-def zslab_slices(g: Geometry, spec: VolumeSpec, batch: int, device) -> int:
-    """z-slab size for host-resident calls: CTPROJ_ZSLAB if set, else 0 (no
-    slabbing) when volume + sinogram + workspaces fit in 80% of the free
-    device memory, else the largest slab that does (north_star item 3)."""
-    import os
-
-    torch = _torch()
-    forced = int(os.environ.get("CTPROJ_ZSLAB", "0"))
-    if forced > 0:
-        return forced
-    vol = 4 * batch * spec.num_voxels
-    sino = 4 * batch * int(np.prod(g.shape))
-    free = torch.cuda.mem_get_info(device)[0]
-    budget = 0.8 * free
-    if 2 * vol + 2 * sino <= budget:
-        return 0
-    per_slice = 2 * vol / spec.numZ
-    room = budget - 2 * sino
-    if room <= per_slice:
-        raise CudaRuntimeError(
-            f"sinogram of {sino / 2**30:.1f} GiB does not fit next to one z-slice on the device")
-    return max(1, int(room // per_slice))

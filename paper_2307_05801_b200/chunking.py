@@ -1,29 +1,34 @@
-"""View-chunked streaming between host memory and the device.
+"""Streaming between host memory and the device: view chunks x z-slabs.
 
 The reference bounds memory by processing one batch element at a time
-(operator.py:59-75) and keeps "one copy of the projection data and volume
-data".  Here the host<->device traffic of a host-resident call
-is split into view chunks so copies overlap the kernels:
+(operator.py:59-66) and keeps "one copy of the projection data and volume
+data".  Here a host-resident call is cut into blocks of
+(z-slab of the volume) x (view chunk of the sinogram), each an ordinary plan
+over ``slab_spec`` / ``Geometry.with_views``, so the device only ever holds
+two slabs, two view chunks and one kernel workspace -- whatever the sizes of
+the volume and the sinogram (north_star item 3):
 
-* forward  (host volume -> host sinogram): the volume goes up once, then
-  chunk k of views is projected on the compute stream while chunk k-1 is
-  copied down on a copy stream into pinned host memory;
-* back     (host sinogram -> host volume): chunk k+1 of views is copied up on
-  the copy stream while chunk k is back-projected into the resident volume
-  with CTP_FLAG_ACCUMULATE; the volume comes down once at the end.
+* forward (host volume -> host sinogram): for each view chunk, the slabs are
+  uploaded in turn (copy stream, double-buffered) and projected into the
+  chunk with CTP_FLAG_ACCUMULATE; the finished chunk is copied down on a
+  second copy stream while the next chunk is projected.  With one slab the
+  volume goes up once;
+* back (host sinogram -> host volume): for each slab, the view chunks are
+  uploaded in turn and back-projected into the slab with CTP_FLAG_ACCUMULATE;
+  the finished slab is copied down while the next slab is computed.  With one
+  view chunk the sinogram goes up once.
 
-Every chunk is a plan over ``Geometry.with_views`` of a contiguous view
-range, so the arithmetic per view is identical to the unchunked call
-(forward: bitwise; back: the per-voxel view sum is split into chunk partial
-sums, i.e. a different fp32 summation order).
+Every device buffer is a slot of a two-entry ring; an upload into a slot waits
+for the event of the kernel that last read it, a kernel writing a slot waits
+for the download that last read it, so the streams never race on recycled
+memory (the caching allocator may hand out blocks still in use on
+another stream).
 
-z-slabs (``zslab_apply``) bound the device working set by the volume side:
-the grid is cut into slabs of ``nzs`` slices (each a plan over a VolumeSpec
-with the slab's numZ / offsetZ).  Forward: slab k+1 is uploaded while slab k is
-projected and accumulated into the resident sinogram (CTP_FLAG_ACCUMULATE).
-Back: slab k is back-projected from the resident sinogram while slab k-1 is
-copied down.  Only one slab of the volume is on the device at a time (two
-while overlapping).
+``plan_blocks`` picks the sizes from a device budget: CTPROJ_DEVICE_BUDGET
+(bytes) if set, else 80% of the free device memory; CTPROJ_ZSLAB forces a
+slab size, CTPROJ_CHUNK_BYTES / CTPROJ_MAX_CHUNKS tune the view chunks.
+Forward with one slab is bitwise identical to one resident call; slabs and
+back chunks only change the fp32 summation order (tested < 1e-6).
 """
 
 from __future__ import annotations
@@ -32,9 +37,13 @@ import math
 import os
 
 from . import _native
+from .errors import CudaRuntimeError
 
-#: target bytes of sinogram per chunk (host<->device granularity)
+#: target bytes of sinogram per view chunk (host<->device granularity)
 CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
+#: at most this many view chunks per call when everything fits: each chunk is
+#: one launch, and a back-projection launch re-reads / re-writes its slab
+MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "8"))
 
 
 def _torch():
@@ -56,81 +65,6 @@ def view_chunks(nv: int, view_bytes: int, chunk_bytes: int = CHUNK_BYTES):
     return [(a, min(nv, a + per)) for a in range(0, nv, per)]
 
 
-def chunk_plans(plan: "_native.Plan", ranges):
-    g, spec, dev = plan.geometry, plan.spec, plan.device.index
-    if len(ranges) == 1:
-        return [plan]
-    return [_native.get_plan(g.with_views(range(a, b)), spec, dev) for a, b in ranges]
-
-
-#: at most this many view chunks per call: each chunk is one kernel launch, and
-#: a back-projection launch re-reads and re-writes the accumulated volume
-MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "8"))
-
-
-def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int | None = None):
-    """Apply A (direction 0) / A^T (1) to a host f32 tensor [B, ...]; returns
-    a pinned host tensor.  The whole batch moves together (so batched paths
-    such as the fan-beam kernels apply); views are chunked by bytes
-    (``CHUNK_BYTES``, or more per chunk so there are at most ``MAX_CHUNKS``)."""
-    torch = _torch()
-    dev = plan.device
-    B = int(host.shape[0])
-    nv, nr, nc = plan.sino_shape
-    view_bytes = B * nr * nc * 4
-    if chunk_bytes is None:
-        chunk_bytes = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
-    ranges = view_chunks(nv, view_bytes, chunk_bytes)
-    plans = chunk_plans(plan, ranges)
-    compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    src = host if host.is_pinned() else host.pin_memory()
-    # one device buffer for the whole sinogram (chunks are slices of it when
-    # B == 1, where a view range is contiguous): no per-chunk allocations, so
-    # repeated calls reuse the same caching-allocator blocks
-    whole = B == 1
-    with torch.cuda.device(dev):
-        if direction == 0:
-            out = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, pin_memory=True)
-            xd = src.to(dev, non_blocking=True)
-            yall = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, device=dev) if whole else None
-            for (a, e), p in zip(ranges, plans):
-                yd = p.forward(xd, out=yall[:, a:e]) if whole else p.forward(xd)
-                ev = torch.cuda.Event()
-                ev.record(compute)
-                copy.wait_event(ev)
-                with torch.cuda.stream(copy):
-                    if len(ranges) == 1:
-                        out.copy_(yd, non_blocking=True)
-                    else:
-                        out[:, a:e].copy_(yd, non_blocking=True)
-                    if not whole:
-                        yd.record_stream(copy)
-            compute.wait_stream(copy)
-            compute.synchronize()
-            return out
-        out_d = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, device=dev)
-        yall = torch.empty((B,) + tuple(plan.sino_shape), dtype=torch.float32, device=dev) if whole else None
-        for k, ((a, e), p) in enumerate(zip(ranges, plans)):
-            with torch.cuda.stream(copy):
-                part = src if len(ranges) == 1 else src[:, a:e]
-                if whole:
-                    yd = yall[:, a:e]
-                    yd.copy_(part, non_blocking=True)
-                else:
-                    yd = part.to(dev, non_blocking=True).contiguous()
-            ev = torch.cuda.Event()
-            ev.record(copy)
-            compute.wait_event(ev)
-            if not whole:
-                yd.record_stream(compute)
-            p.back(yd, out=out_d, accumulate=k > 0)
-        out = torch.empty((B,) + tuple(plan.vol_shape), dtype=torch.float32, pin_memory=True)
-        out.copy_(out_d, non_blocking=True)
-        compute.synchronize()
-        return out
-
-
 def slab_spec(spec, z_first: int, nzs: int):
     """VolumeSpec of slices [z_first, z_first + nzs) of ``spec``."""
     from .geometry import VolumeSpec
@@ -146,45 +80,221 @@ def zslab_ranges(nz: int, nzs: int):
     return [(a, min(nz, a + nzs)) for a in range(0, nz, nzs)]
 
 
-def zslab_apply(plan: "_native.Plan", host, direction: int, nzs: int):
-    """Host tensor in -> pinned host tensor out, streaming the volume in
-    z-slabs of ``nzs`` slices (see module docstring)."""
+def device_budget(device) -> int:
+    """Bytes a streamed call may hold on ``device``."""
+    forced = int(os.environ.get("CTPROJ_DEVICE_BUDGET", "0"))
+    if forced > 0:
+        return forced
+    torch = _torch()
+    return int(0.8 * torch.cuda.mem_get_info(device)[0])
+
+
+def block_bytes(g, spec, batch: int, nzs: int, nvc: int) -> int:
+    """Device bytes a streamed call holds for slabs of ``nzs`` slices and view
+    chunks of ``nvc`` views: two slab slots + two chunk slots + the larger
+    kernel workspace (a transposed copy of the launch's input, ctp_sf_*)."""
+    xs = 4 * batch * spec.numX * spec.numY * nzs
+    yc = 4 * batch * nvc * g.detector.numRows * g.detector.numCols
+    return 2 * xs + 2 * yc + max(xs, yc)
+
+
+def plan_blocks(g, spec, batch: int, budget: int):
+    """(nzs, view ranges) for a streamed call within ``budget`` bytes: the
+    whole volume with up to MAX_CHUNKS view chunks (or 32-view chunks) when
+    that fits; otherwise z-slabs with the largest view chunks that still leave
+    room for at least one slice (down to single views)."""
+    nv, nz = g.numViews, spec.numZ
+    view_bytes = 4 * batch * g.detector.numRows * g.detector.numCols
+    slice_bytes = 4 * batch * spec.numX * spec.numY
+    forced = int(os.environ.get("CTPROJ_ZSLAB", "0"))
+    chunk = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
+    options = []
+    for nvc_cap in (chunk // view_bytes, 32, 1):
+        ranges = view_chunks(nv, view_bytes, max(1, nvc_cap) * view_bytes)
+        nvc = max(b - a for a, b in ranges)
+        if forced > 0:
+            nzs = min(forced, nz)
+        else:
+            room = budget - 3 * nvc * view_bytes  # 2 chunk slots + (at most) a chunk workspace
+            nzs = min(nz, room // (3 * slice_bytes)) if room > 0 else 0
+        if nzs >= 1 and (forced > 0 or block_bytes(g, spec, batch, nzs, nvc) <= budget):
+            options.append((int(nzs), ranges))
+    if forced > 0 and options:
+        return options[0]
+    # whole volume with chunks of >= 32 views (the back kernel sets up 32 views
+    # per pass); then the largest chunks that leave room for some slabs
+    for nzs, ranges in options:
+        if nzs == nz and (len(ranges) == 1 or ranges[0][1] - ranges[0][0] >= 32):
+            return nzs, ranges
+    if options:
+        return options[0]
+    raise CudaRuntimeError(
+        f"cannot stream within {budget / 2**30:.2f} GiB: one z-slice ({slice_bytes} B) and one view "
+        f"({view_bytes} B) per block need {block_bytes(g, spec, batch, 1, 1)} B")
+
+
+def _flat(buf, shape):
+    """Contiguous view of the first prod(shape) elements of a flat buffer."""
+    n = 1
+    for s in shape:
+        n *= int(s)
+    return buf[:n].view(shape)
+
+
+def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = None, ranges=None):
+    """Apply A (direction 0) / A^T (1) of ``plan`` to a host f32 tensor
+    [B, ...] block by block (z-slabs of ``nzs`` slices x view ``ranges``);
+    returns a pinned host tensor."""
     torch = _torch()
     dev = plan.device
     g, spec = plan.geometry, plan.spec
     B = int(host.shape[0])
-    ranges = zslab_ranges(spec.numZ, nzs)
-    plans = [_native.get_plan(g, slab_spec(spec, a, b - a), dev.index) for a, b in ranges]
+    nz, ny, nx = spec.shape
+    nv, nr, nc = g.shape
+    if nzs is None or ranges is None:
+        nzs0, ranges0 = plan_blocks(g, spec, B, device_budget(dev))
+        nzs = nzs0 if nzs is None else nzs
+        ranges = ranges0 if ranges is None else ranges
+    zr = zslab_ranges(nz, min(nzs, nz))
+    one_slab, one_chunk = len(zr) == 1, len(ranges) == 1
+    plans = {}
+
+    def sub(zi, vi):
+        key = (zi, vi)
+        if key not in plans:
+            if one_slab and one_chunk:
+                plans[key] = plan
+            else:
+                (z0, z1), (a, e) = zr[zi], ranges[vi]
+                gg = g if one_chunk else g.with_views(range(a, e))
+                ss = spec if one_slab else slab_spec(spec, z0, z1 - z0)
+                plans[key] = _native.get_plan(gg, ss, dev.index)
+        return plans[key]
+
     compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     src = host if host.is_pinned() else host.pin_memory()
+    nzs_max = max(z1 - z0 for z0, z1 in zr)
+    nvc_max = max(e - a for a, e in ranges)
+
+    def upload(dst, zi_or_vi, slab):
+        """dst (device) <- the host block; per batch element when strided."""
+        with torch.cuda.stream(h2d):
+            if slab:
+                z0, z1 = zr[zi_or_vi]
+                part = src if one_slab else src[:, z0:z1]
+            else:
+                a, e = ranges[zi_or_vi]
+                part = src if one_chunk else src[:, a:e]
+            if B == 1 or part.is_contiguous():
+                dst.copy_(part, non_blocking=True)
+            else:
+                for b in range(B):
+                    dst[b].copy_(part[b], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(h2d)
+        compute.wait_event(ev)
+
+    def download(out, block, sl):
+        ev = torch.cuda.Event()
+        ev.record(compute)
+        d2h.wait_event(ev)
+        with torch.cuda.stream(d2h):
+            dst = out if sl is None else out[:, sl[0]:sl[1]]
+            if B == 1 or dst.is_contiguous():
+                dst.copy_(block, non_blocking=True)
+            else:
+                for b in range(B):
+                    dst[b].copy_(block[b], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(d2h)
+        return done
+
     with torch.cuda.device(dev):
         if direction == 0:
-            yd = torch.zeros((B,) + tuple(g.shape), dtype=torch.float32, device=dev)
-            for b in range(B):
-                for k, ((a, e), p) in enumerate(zip(ranges, plans)):
-                    with torch.cuda.stream(copy):
-                        xs = src[b:b + 1, a:e].to(dev, non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(copy)
-                    compute.wait_event(ev)
-                    xs.record_stream(compute)
-                    p.forward(xs, out=yd[b:b + 1], accumulate=True)
-            out = torch.empty((B,) + tuple(g.shape), dtype=torch.float32, pin_memory=True)
-            out.copy_(yd, non_blocking=True)
+            out = torch.empty((B, nv, nr, nc), dtype=torch.float32, pin_memory=True)
+            yring = [torch.empty(B * nvc_max * nr * nc, dtype=torch.float32, device=dev) for _ in range(2)]
+            y_free = [None, None]  # download that last read the slot
+            if one_slab:
+                xd = torch.empty((B, nz, ny, nx), dtype=torch.float32, device=dev)
+                upload(xd, 0, True)
+            else:
+                xring = [torch.empty(B * nzs_max * ny * nx, dtype=torch.float32, device=dev) for _ in range(2)]
+                x_free = [None, None]  # kernel that last read the slot
+            step = 0
+            for vi, (a, e) in enumerate(ranges):
+                k = vi % 2
+                ys = _flat(yring[k], (B, e - a, nr, nc))
+                if y_free[k] is not None:
+                    compute.wait_event(y_free[k])
+                for zi, (z0, z1) in enumerate(zr):
+                    if one_slab:
+                        xs = xd
+                    else:
+                        s = step % 2
+                        if x_free[s] is not None:
+                            h2d.wait_event(x_free[s])
+                        xs = _flat(xring[s], (B, z1 - z0, ny, nx))
+                        upload(xs, zi, True)
+                    sub(zi, vi).forward(xs, out=ys, accumulate=zi > 0)
+                    if not one_slab:
+                        x_free[s] = torch.cuda.Event()
+                        x_free[s].record(compute)
+                        step += 1
+                y_free[k] = download(out, ys, None if one_chunk else (a, e))
+            compute.wait_stream(d2h)
             compute.synchronize()
             return out
-        yd = src.to(dev, non_blocking=True)
-        out = torch.empty((B,) + tuple(spec.shape), dtype=torch.float32, pin_memory=True)
-        for b in range(B):
-            for (a, e), p in zip(ranges, plans):
-                xs = p.back(yd[b:b + 1])
-                ev = torch.cuda.Event()
-                ev.record(compute)
-                copy.wait_event(ev)
-                with torch.cuda.stream(copy):
-                    out[b, a:e].copy_(xs[0], non_blocking=True)
-                    xs.record_stream(copy)
-        compute.wait_stream(copy)
+        out = torch.empty((B, nz, ny, nx), dtype=torch.float32, pin_memory=True)
+        xring = [torch.empty(B * nzs_max * ny * nx, dtype=torch.float32, device=dev) for _ in range(2)]
+        x_free = [None, None]
+        if one_chunk:
+            yd = torch.empty((B, nv, nr, nc), dtype=torch.float32, device=dev)
+            upload(yd, 0, False)
+        else:
+            yring = [torch.empty(B * nvc_max * nr * nc, dtype=torch.float32, device=dev) for _ in range(2)]
+            y_free = [None, None]
+        step = 0
+        for zi, (z0, z1) in enumerate(zr):
+            k = zi % 2
+            xs = _flat(xring[k], (B, z1 - z0, ny, nx))
+            if x_free[k] is not None:
+                compute.wait_event(x_free[k])
+            for vi, (a, e) in enumerate(ranges):
+                if one_chunk:
+                    ys = yd
+                else:
+                    s = step % 2
+                    if y_free[s] is not None:
+                        h2d.wait_event(y_free[s])
+                    ys = _flat(yring[s], (B, e - a, nr, nc))
+                    upload(ys, vi, False)
+                sub(zi, vi).back(ys, out=xs, accumulate=vi > 0)
+                if not one_chunk:
+                    y_free[s] = torch.cuda.Event()
+                    y_free[s].record(compute)
+                    step += 1
+            x_free[k] = download(out, xs, None if one_slab else (z0, z1))
+        compute.wait_stream(d2h)
         compute.synchronize()
         return out
+
+
+def host_apply(plan: "_native.Plan", host, direction: int, chunk_bytes: int | None = None):
+    """Whole volume resident, views in chunks of about ``chunk_bytes``
+    (default: CHUNK_BYTES, or more so there are at most MAX_CHUNKS)."""
+    B = int(host.shape[0])
+    nv, nr, nc = plan.sino_shape
+    view_bytes = B * nr * nc * 4
+    if chunk_bytes is None:
+        chunk_bytes = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
+    return stream_apply(plan, host, direction, plan.spec.numZ, view_chunks(nv, view_bytes, chunk_bytes))
+
+
+def zslab_apply(plan: "_native.Plan", host, direction: int, nzs: int):
+    """z-slabs of ``nzs`` slices, views in the default chunks."""
+    B = int(host.shape[0])
+    nv, nr, nc = plan.sino_shape
+    view_bytes = B * nr * nc * 4
+    chunk_bytes = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
+    return stream_apply(plan, host, direction, nzs, view_chunks(nv, view_bytes, chunk_bytes))

@@ -385,9 +385,10 @@ static bool use_fan_path(const ctp_plan* plan, int batch, uint32_t flags) {
 
 size_t ctp_sf_workspace_bytes(const ctp_plan* plan, int direction, int batch) {
   if (!plan || batch < 1) return 0;
-  size_t per = direction == 0 ? plan->vol_elems : plan->sino_elems;
-  if (plan->gp.nz == 1 && plan->gp.nr == 1 && batch >= 2)
-    per = plan->vol_elems + plan->sino_elems;  // both batch-innermost copies
+  // a transposed copy of the input: z-contiguous volume / row-contiguous
+  // sinogram (3D), batch-innermost input (fan; the fan kernels write the
+  // natural output layout directly)
+  const size_t per = direction == 0 ? plan->vol_elems : plan->sino_elems;
   return align_up(per * sizeof(float) * (size_t)batch);
 }
 
@@ -411,15 +412,12 @@ int ctp_sf_forward(const ctp_plan* plan, const float* vol, float* sino, int batc
   const GridParams& gp = plan->gp;
   if (use_fan_path(plan, batch, flags)) {
     float* xB = static_cast<float*>(workspace);
-    float* yB = xB + plan->vol_elems * (size_t)batch;
     cudaError_t e = ctp::launch_transpose(vol, xB, batch, (int)plan->vol_elems, 1, s);
     if (e != cudaSuccess) return cuda_fail(e, "transpose volume (fan)");
     KernelTimer timer(plan, 0, s, flags);
-    e = ctp::launch_forward_fan(gp, plan->d_coef, xB, yB, batch, s);
+    e = ctp::launch_forward_fan(gp, plan->d_coef, xB, sino, batch, s);
     timer.stop();
     if (e != cudaSuccess) return cuda_fail(e, "sf_forward_fan_kernel");
-    e = ctp::launch_transpose(yB, sino, (int)plan->sino_elems, batch, 1, s);
-    if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram (fan)");
     return CTP_OK;
   }
   float* xT = static_cast<float*>(workspace);
@@ -444,15 +442,12 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
   const GridParams& gp = plan->gp;
   if (use_fan_path(plan, batch, flags)) {
     float* yB = static_cast<float*>(workspace);
-    float* xB = yB + plan->sino_elems * (size_t)batch;
     cudaError_t e = ctp::launch_transpose(sino, yB, batch, (int)plan->sino_elems, 1, s);
     if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram (fan)");
     KernelTimer timer(plan, 1, s, flags);
-    e = ctp::launch_back_fan(gp, plan->d_coef, yB, xB, batch, s);
+    e = ctp::launch_back_fan(gp, plan->d_coef, yB, vol, batch, s);
     timer.stop();
     if (e != cudaSuccess) return cuda_fail(e, "sf_back_fan_kernel");
-    e = ctp::launch_transpose(xB, vol, (int)plan->vol_elems, batch, 1, s);
-    if (e != cudaSuccess) return cuda_fail(e, "transpose volume (fan)");
     return CTP_OK;
   }
   float* yT = static_cast<float*>(workspace);

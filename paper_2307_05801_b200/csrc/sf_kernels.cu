@@ -1233,7 +1233,7 @@ __device__ __forceinline__ float row0_weight(float A, float B, float E, bool& hi
 template <int G>
 __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const ViewCoef* __restrict__ vcoef,
                                                           const float* __restrict__ yB,  // [nv][nc][Bs]
-                                                          float* __restrict__ xB,        // [ny*nx][Bs]
+                                                          float* __restrict__ xo,        // [Bs][ny*nx]
                                                           int Bs, int b0, int nb) {
   __shared__ __align__(16) BkEntry ents[8][32][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1360,7 +1360,9 @@ __global__ void __launch_bounds__(256) sf_back_fan_kernel(GridParams gp, const V
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int b = lane + 32 * g;
-    if (b < nb) xB[(size_t)pix * Bs + b0 + b] = acc[g];
+    // natural layout out[b][iy][ix] (lane stride ny*nx: one 4-byte store per
+    // lane, but no batch-innermost copy of the volume in the workspace)
+    if (b < nb) xo[(size_t)(b0 + b) * ((size_t)gp.nx * gp.ny) + pix] = acc[g];
   }
 }
 
@@ -1417,7 +1419,7 @@ __device__ __noinline__ int fan_candidates(const GridParams& gp, const ViewCoef*
 template <int G>
 __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const float* __restrict__ xB,  // [ny*nx][Bs]
-    float* __restrict__ yB,                                                         // [nv][nc][Bs]
+    float* __restrict__ yo,                                                         // [Bs][nv][nc]
     int Bs, int b0, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1516,14 +1518,16 @@ __global__ void __launch_bounds__(FV_WARPS * 32) sf_forward_fan_kernel(
     }
   }
   if (pending > 0) flush();
-  float* yv = yB + (size_t)v * gp.nc * Bs + b0;
+  // natural layout y[b][v][c0 .. c0 + 3] (16 contiguous bytes per lane, no
+  // batch-innermost copy of the sinogram in the workspace)
+  float* yv = yo + (size_t)v * gp.nc + c0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int b = lane + 32 * g;
     if (b >= nb) continue;
 #pragma unroll
     for (int c = 0; c < FW_CW; ++c)
-      if (c < cw) yv[(size_t)(c0 + c) * Bs + b] = acc[g][c];
+      if (c < cw) yv[(size_t)(b0 + b) * gp.nv * gp.nc + c] = acc[g][c];
   }
 }
 
@@ -1591,8 +1595,8 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const Vi
   return cudaGetLastError();
 }
 
-// xB: [ny*nx][batch]; yB: [nv][nc][batch] (batch-innermost), nz == nr == 1
-cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,
+// xB: [ny*nx][batch] (batch-innermost input); sino: [batch][nv][nc]; nz == nr == 1
+cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* sino,
                                int batch, cudaStream_t st) {
   const size_t smem = sizeof(FwEntry) * FV_EBUF * FV_WARPS;
   const long long ntasks = (long long)((gp.nc + FW_CW - 1) / FW_CW) * gp.nv;
@@ -1606,7 +1610,7 @@ cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, cons
     e = cudaFuncSetAttribute(sf_forward_fan_kernel<g>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                            \
     if (e != cudaSuccess) return e;                                                                 \
-    sf_forward_fan_kernel<g><<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xB, yB, batch, b0, nb); \
+    sf_forward_fan_kernel<g><<<grid, FV_WARPS * 32, smem, st>>>(gp, vcoef, xB, sino, batch, b0, nb); \
     break;
     switch (G) { CTP_FAN_FWD(1) CTP_FAN_FWD(2) CTP_FAN_FWD(3) default: CTP_FAN_FWD(4) }
 #undef CTP_FAN_FWD
@@ -1614,7 +1618,7 @@ cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
+cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* vol,
                             int batch, cudaStream_t st) {
 #if CTP_FB_ALONG_Y
   const unsigned grid = (unsigned)(gp.nx * ((gp.ny + 7) / 8));
@@ -1625,10 +1629,10 @@ cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const f
     const int nb = min(32 * F2_MAXG, batch - b0);
     const int G = (nb + 31) / 32;
     switch (G) {
-      case 1: sf_back_fan_kernel<1><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
-      case 2: sf_back_fan_kernel<2><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
-      case 3: sf_back_fan_kernel<3><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
-      default: sf_back_fan_kernel<4><<<grid, 256, 0, st>>>(gp, vcoef, yB, xB, batch, b0, nb); break;
+      case 1: sf_back_fan_kernel<1><<<grid, 256, 0, st>>>(gp, vcoef, yB, vol, batch, b0, nb); break;
+      case 2: sf_back_fan_kernel<2><<<grid, 256, 0, st>>>(gp, vcoef, yB, vol, batch, b0, nb); break;
+      case 3: sf_back_fan_kernel<3><<<grid, 256, 0, st>>>(gp, vcoef, yB, vol, batch, b0, nb); break;
+      default: sf_back_fan_kernel<4><<<grid, 256, 0, st>>>(gp, vcoef, yB, vol, batch, b0, nb); break;
     }
   }
   return cudaGetLastError();

@@ -22,10 +22,12 @@ constexpr int kBackZBlock = 256;  // slices per back-kernel z-block (BK_ZC)
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
                         float* vol, int batch, bool accumulate, cudaStream_t st, int z0 = 0, int z1 = -1);
 size_t forward_warp_smem_bytes();
-// fan beam (nz == nr == 1) with the batch innermost: xB [ny*nx][batch], yB [nv][nc][batch]
-cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* yB,
+// fan beam (nz == nr == 1) with the batch on the lanes: inputs batch-innermost
+// (xB [ny*nx][batch], yB [nv][nc][batch]), outputs in the natural layouts
+// (sino [batch][nv][nc], vol [batch][ny*nx])
+cudaError_t launch_forward_fan(const GridParams& gp, const ViewCoef* vcoef, const float* xB, float* sino,
                                int batch, cudaStream_t st);
-cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* xB,
+cudaError_t launch_back_fan(const GridParams& gp, const ViewCoef* vcoef, const float* yB, float* vol,
                             int batch, cudaStream_t st);
 
 // Siddon pair (siddon_kernels.cu): the float64 scalars of kernel_geom

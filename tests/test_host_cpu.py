@@ -224,3 +224,26 @@ def test_capi_validates_before_touching_the_device():
     # the Siddon entry points validate the same way
     assert lib.ctp_siddon_forward(None, 1.0, None, None, 1, 0, None) == 1
     assert lib.ctp_siddon_back(None, 1.0, None, None, 1, 0, None) == 1
+
+
+def test_stream_planner_respects_budget():
+    """chunking.plan_blocks: view chunks, then z-slabs, within the budget."""
+    from paper_2307_05801_b200 import chunking
+
+    g, spec = ct.parse_config(json.dumps(dict(
+        geometry="cone", numX=512, numY=512, numZ=512, voxelWidth=0.6667, voxelHeight=0.6667,
+        numRows=768, numCols=768, pixelHeight=1.0, pixelWidth=1.0, sod=1000.0, sdd=1500.0,
+        numAngles=720, angularRange=360.0)))
+    big = 64 << 30
+    nzs, ranges = chunking.plan_blocks(g, spec, 1, big)
+    assert nzs == 512 and len(ranges) <= chunking.MAX_CHUNKS
+    for budget in (1 << 30, 256 << 20, 40 << 20):
+        nzs, ranges = chunking.plan_blocks(g, spec, 1, budget)
+        nvc = max(b - a for a, b in ranges)
+        assert chunking.block_bytes(g, spec, 1, nzs, nvc) <= budget
+        assert ranges[0][0] == 0 and ranges[-1][1] == 720
+        assert all(r1[1] == r2[0] for r1, r2 in zip(ranges, ranges[1:]))
+    nzs, _ = chunking.plan_blocks(g, spec, 1, 40 << 20)
+    assert nzs < 512  # the volume no longer fits: z-slabs
+    with pytest.raises(ct.CudaRuntimeError):
+        chunking.plan_blocks(g, spec, 1, 1 << 20)
