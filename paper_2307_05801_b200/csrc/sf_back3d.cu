@@ -1,0 +1,588 @@
+// sf_back3d.cu -- 3D back projection x = A^T y of the SF-TR pair (parallel,
+// cone flat/curved, SF-modular), voxel-driven GATHER (reference:
+// sf_back_kernel, _kernels.py:666-763).
+//
+// Integral formulation.  For one voxel column (ix, iy) in one view the axial
+// footprints of consecutive slices TILE the detector column: slice i spans
+// rows [W0 + B i, W0 + B (i + 1)) (row units, B = mag hz / ph), so
+//
+//   x[i] += amp_i * sum_r overlap(slice i, row r) * Q(r),   Q(r) = sum_c ts(c) y[c][r]
+//         = amp_i * (H(w_{i+1}) - H(w_i)),
+//
+// where H is the integral of the piecewise-constant row profile Q:
+// H(w) = S_k + (w - k) Q_k, k = floor(w), S_k = sum_{j<k} Q_j.  The reference
+// sums tt(r) Q(r) over the 2-3 rows a slice touches (_kernels.py:738-760);
+// here a warp builds the (S, Q) table of the rows its slices reach once per
+// view (coalesced 16-byte loads along the row-contiguous sinogram, warp
+// prefix scan) and every slice costs ONE table evaluation: lanes own slices
+// lane + 32 m, each lane evaluates H at the upper boundary of its slice and
+// takes the lower one from lane - 1 with a shuffle.  Mathematically identical
+// to the reference; in fp32 the prefix sums cost ~log2(rows) bits of the
+// per-slice difference (relative error ~1e-5 per view, well inside the 1e-4
+// bar, tests/test_gpu_parity.py).
+//
+// Footprint setup is lane-parallel (lane l sets up view vb + l, as in round
+// 1): transverse trapezoid and column weights in fp32 (sf_common.cuh), axial
+// map in f64 at the (sub-)voxel centre, stored relative to the table origin.
+// Entries the table path cannot take (footprints wider than 4 columns, the
+// second half of a split voxel, tables longer than B3_QMAX rows) take the
+// direct per-row path.  No atomics: one lane owns each output voxel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "sf_common.cuh"
+#include "sf_launch.h"
+
+#ifndef CTP_B3_WARPS
+#define CTP_B3_WARPS 8
+#endif
+#ifndef CTP_B3_MINB
+#define CTP_B3_MINB 3
+#endif
+// rare paths (split halves, direct rows) inlined into the view loop: keeps the
+// accumulators in place (no phi copies), at the cost of code size
+#ifndef CTP_B3_INLINE_RARE
+#define CTP_B3_INLINE_RARE 1
+#endif
+#if CTP_B3_INLINE_RARE
+#define CTP_B3_RARE __forceinline__
+#else
+#define CTP_B3_RARE __noinline__
+#endif
+
+namespace ctp {
+
+constexpr int B3_WARPS = CTP_B3_WARPS;  // warps per CTA: a 1 x B3_WARPS strip of voxel columns along y
+constexpr int B3_NCF = 4;               // footprint columns of the table path
+
+template <int ZPL>
+struct B3Cfg {
+  static constexpr int ZC = 32 * ZPL;  // slices per warp (lanes own lane + 32 m)
+  // table rows: slices of B <= 1.5 rows plus margins, in whole 128-row chunks
+  static constexpr int QMAX = ((ZC * 3 / 2 + 8) + 127) / 128 * 128;
+};
+
+struct B3Entry {  // one (sub-)voxel footprint of the warp's column in one view
+  float W0;       // lower boundary of slice izs + 0.5, relative to the table origin R0
+  float B;        // rows per slice
+  float A;        // centre of slice izs relative to R0 (direct path)
+  float lxy;
+  float a0, a1;   // amp(i) = lxy sqrt(1 + (a0 + a1 i)^2), i = iz - izs
+  int cl, ncol;   // footprint columns cl .. cl + ncol - 1 (ncol 0: no contribution)
+  float ts[B3_NCF];
+  int R0;         // table origin: absolute row, multiple of 4
+  int n4;         // table rows / 4 (0: direct path)
+  int mask;       // sub-footprints of this view (bit 1: second half of a split voxel)
+  int pad;       // S table base - 2^23 entries (shared address; see b3_eval)
+};
+static_assert(sizeof(B3Entry) == 64, "B3Entry layout");
+
+template <int ZPL>
+struct B3Smem {
+  B3Entry ents[B3_WARPS][32];
+  B3Entry split[B3_WARPS];
+  float tab[B3_WARPS][2][B3Cfg<ZPL>::QMAX];  // [0]: S_k, [1]: Q_k of the table rows
+};
+
+// Footprint of one (sub-)voxel for slices izs..ize: f64 axial map at the
+// centre cxy, table origin and length, fp32 column weights.
+template <int ZPL>
+__device__ __forceinline__ void b3_fill(B3Entry& e, const SubFoot& f, const GridParams& gp, int izs, int ize,
+                                        const ViewAx& ax, float2 cxy) {
+  e.lxy = f.lxy;
+  e.a1 = f.a1;
+  e.a0 = fma_(f.a1, (float)izs, f.a0);
+  e.cl = f.cl;
+  e.ncol = f.ch >= f.cl ? f.ch - f.cl + 1 : 0;
+  const Trap p = make_trap(f);
+  float ts[B3_NCF];
+  col_weights<B3_NCF>(p, f.cl, ts);
+#pragma unroll
+  for (int k = 0; k < B3_NCF; ++k) e.ts[k] = k < e.ncol ? ts[k] : 0.0f;
+  double A, B;
+  axial64(ax, gp.kind, (double)cxy.x, (double)cxy.y, A, B);
+  const double Ts = fma(B, (double)izs, A), Te = fma(B, (double)ize, A);
+  const double lo = Ts - 0.5 * B, hi = Te + 0.5 * B;
+  // rows touched: row r spans [r - .5, r + .5)
+  const double fa = floor(lo + 0.5), fz = floor(hi + 0.5);
+  if (fz < 0.0 || fa > (double)(gp.nr - 1)) {  // entirely off the detector
+    e.ncol = 0;
+    e.n4 = 0;
+    e.R0 = 0;
+    e.W0 = e.B = e.A = 0.0f;
+    return;
+  }
+  const int Ra = (int)fmax(fa, -1.0e6), Rz = (int)fmin(fz, 1.0e6);
+  // origin one row below the first touched row (every boundary w >= 1, far
+  // from the k = -1 edge under fp32 rounding), table one row past the last
+  const int R0 = (Ra - 1) & ~3;
+  const int n4 = (Rz - R0 + 2 + 3) >> 2;
+  e.R0 = R0;
+  e.W0 = (float)(lo + 0.5 - (double)R0);
+  e.B = (float)B;
+  e.A = (float)(Ts - (double)R0);
+  const bool fast = e.ncol >= 1 && e.ncol <= B3_NCF && 4 * n4 <= B3Cfg<ZPL>::QMAX;
+  e.n4 = fast ? n4 : 0;
+}
+
+// Lane-parallel setup of views vb + lane; the first sub-footprint goes to *e
+// (the second half of a split voxel is rebuilt in the view loop).  Returns
+// whether any view of the 32 splits the voxel.  Out of line: its registers
+// stay out of the view loop's allocation.
+template <int ZPL>
+__device__ __noinline__ bool b3_setup(const GridParams& gp, const ViewCoef* __restrict__ vcoef,
+                                      const ViewAx* __restrict__ vax, int vb, int ix, int iy, int izs, int ize,
+                                      B3Entry* e, unsigned tab_adj) {
+  const int v = vb + (threadIdx.x & 31);
+  B3Entry E;
+  E.ncol = 0;
+  E.n4 = 0;
+  E.R0 = 0;
+  int mask = 0;
+  if (v < gp.nv) {
+    const ViewCoef vc = vcoef[v];
+    SubFoot f0, f1;
+    float2 c0, c1;
+    mask = column_subs(vc, gp, ix, iy, f0, f1, c0, c1) & 3;
+    if (mask & 1) b3_fill<ZPL>(E, f0, gp, izs, ize, vax[v], c0);
+  }
+  E.mask = mask;
+  E.pad = (int)tab_adj;
+  *e = E;
+  return __any_sync(0xffffffffu, (mask & 2) != 0);
+}
+
+// Second half of a split voxel (_sf_subdivide, _kernels.py:542-552), rebuilt
+// by one lane when a view needs it.
+template <int ZPL>
+__device__ CTP_B3_RARE void b3_split(const GridParams& gp, const ViewCoef* __restrict__ vcoef,
+                                      const ViewAx* __restrict__ vax, int v, int ix, int iy, int izs, int ize,
+                                      B3Entry* e, unsigned tab_adj) {
+  SubFoot f0, f1;
+  float2 c0, c1;
+  const int mask = column_subs(vcoef[v], gp, ix, iy, f0, f1, c0, c1);
+  B3Entry E;
+  E.ncol = 0;
+  E.n4 = 0;
+  E.R0 = 0;
+  E.mask = 0;
+  if (mask & 2) b3_fill<ZPL>(E, f1, gp, izs, ize, vax[v], c1);
+  E.pad = (int)tab_adj;
+  *e = E;
+}
+
+// ---- table: (S_k, Q_k) of rows R0 + k, k < 4 n4 --------------------------
+// Lane t builds rows 4 (32 c + t) .. + 3 of chunk c (one 16-byte load per
+// footprint column when VEC), local prefix, warp scan of the group totals,
+// running carry across chunks.  Groups outside the detector read 0 (with
+// VEC, R0 and nr are multiples of 4, so a group is entirely in or out).
+template <int NC, bool VEC, int QMAX>
+__device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const float* __restrict__ yc, int nr,
+                                                 int R0, int n4, const float (&ts)[B3_NCF], int lane) {
+  float carry = 0.0f;
+  const int nch = (n4 + 31) >> 5;
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    const int g = (c << 5) + lane;
+    const int r = R0 + 4 * g;
+    float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (g < n4) {
+      if (VEC) {
+        if (r >= 0 && r < nr) {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(yc + (size_t)k * nr + r));
+            q[0] = fmaf(ts[k], a.x, q[0]);
+            q[1] = fmaf(ts[k], a.y, q[1]);
+            q[2] = fmaf(ts[k], a.z, q[2]);
+            q[3] = fmaf(ts[k], a.w, q[3]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = r + i;
+          if (rr >= 0 && rr < nr) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) q[i] = fmaf(ts[k], __ldg(yc + (size_t)k * nr + rr), q[i]);
+          }
+        }
+      }
+    }
+    const float s1 = q[0], s2 = s1 + q[1], s3 = s2 + q[2], tot = s3 + q[3];
+    float incl = tot;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float n = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += n;
+    }
+    const float ex = carry + (incl - tot);
+    if (g < QMAX / 4) {
+      reinterpret_cast<float4*>(tab)[g] = make_float4(ex, ex + s1, ex + s2, ex + s3);
+      reinterpret_cast<float4*>(tab + QMAX)[g] = make_float4(q[0], q[1], q[2], q[3]);
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// Fast table (16-byte aligned rows, every table row on the detector): lane t
+// builds rows 256 c + 4 t .. + 3 (half 0) and 256 c + 128 + 4 t .. + 3 (half
+// 1) of chunk c, so every 16-byte load and store instruction covers 512
+// contiguous bytes (no bank conflicts, 4 wavefronts); two independent warp
+// scans per chunk.  Column pointers are per lane, chunks are unrolled and
+// addressed with immediate offsets.
+template <int NC, int NCH, int QMAX>
+__device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const float* __restrict__ yc, int nr, int nq,
+                                              const float (&ts)[B3_NCF], int lane) {
+  const float* p[NC];
+  float2 T[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    p[k] = yc + k * nr + 4 * lane;
+    T[k] = bc2_(ts[k]);
+  }
+  float4* sp4 = reinterpret_cast<float4*>(tab + 4 * lane);
+  float4* qp4 = reinterpret_cast<float4*>(tab + QMAX + 4 * lane);
+  float carry = 0.0f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (256 * c >= nq) break;  // warp-uniform
+    const bool ok0 = 256 * c + 4 * lane < nq, ok1 = 256 * c + 128 + 4 * lane < nq;
+    float2 q0 = make_float2(0.0f, 0.0f), q1 = q0, q2 = q0, q3 = q0;  // half 0: q0 q1, half 1: q2 q3
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      if (ok0) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p[k] + 256 * c));
+        q0 = fma2_(T[k], make_float2(a.x, a.y), q0);
+        q1 = fma2_(T[k], make_float2(a.z, a.w), q1);
+      }
+      if (ok1) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p[k] + 256 * c + 128));
+        q2 = fma2_(T[k], make_float2(b.x, b.y), q2);
+        q3 = fma2_(T[k], make_float2(b.z, b.w), q3);
+      }
+    }
+    // exclusive prefixes of the lane's two 4-row groups, two warp scans
+    const float a1 = q0.x, a2 = a1 + q0.y, a3 = a2 + q1.x, ta = a3 + q1.y;
+    const float b1 = q2.x, b2 = b1 + q2.y, b3 = b2 + q3.x, tb = b3 + q3.y;
+    float ia = ta, ib = tb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float na = __shfl_up_sync(0xffffffffu, ia, d);
+      const float nb = __shfl_up_sync(0xffffffffu, ib, d);
+      if (lane >= d) {
+        ia += na;
+        ib += nb;
+      }
+    }
+    const float tot_a = __shfl_sync(0xffffffffu, ia, 31);
+    const float tot_b = __shfl_sync(0xffffffffu, ib, 31);
+    const float ea = carry + (ia - ta), eb = (carry + tot_a) + (ib - tb);
+    const float2 e01 = add2_(bc2_(ea), make_float2(0.0f, a1)), e23 = add2_(bc2_(ea), make_float2(a2, a3));
+    const float2 f01 = add2_(bc2_(eb), make_float2(0.0f, b1)), f23 = add2_(bc2_(eb), make_float2(b2, b3));
+    if (ok0) {  // (rows past nq are never evaluated; the arrays end at QMAX)
+      sp4[64 * c] = make_float4(e01.x, e01.y, e23.x, e23.y);
+      qp4[64 * c] = make_float4(q0.x, q0.y, q1.x, q1.y);
+    }
+    if (ok1) {
+      sp4[64 * c + 32] = make_float4(f01.x, f01.y, f23.x, f23.y);
+      qp4[64 * c + 32] = make_float4(q2.x, q2.y, q3.x, q3.y);
+    }
+    carry += tot_a + tot_b;
+  }
+}
+
+template <int QMAX>
+__device__ __forceinline__ float b3_eval(unsigned tab_adj, float w) {
+  const float tf = __fadd_rd(w, 8388608.0f);
+  const float fr = w - (tf - 8388608.0f);  // both subtractions exact
+  const unsigned a = (unsigned)__float_as_int(tf) * 4u + tab_adj;  // one LEA
+  float S, Q;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q) : "r"(a), "n"(4 * QMAX));
+  return fmaf(fr, Q, S);
+}
+
+__device__ __forceinline__ float2 sub2_(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// (a + 2^23) rounded toward -inf, packed
+__device__ __forceinline__ float2 add_rm_2p23_2_(float2 a) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\t"
+      "add.rm.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(8388608.0f));
+  return d;
+}
+
+// Table lookups of a pair of boundaries (packed floor trick)
+template <int QMAX>
+__device__ __forceinline__ float2 b3_eval2(unsigned tab_adj, float2 w) {
+  const float2 tf = add_rm_2p23_2_(w);
+  const float2 fr = sub2_(w, add2_(tf, bc2_(-8388608.0f)));  // exact
+  const unsigned a0 = (unsigned)__float_as_int(tf.x) * 4u + tab_adj;
+  const unsigned a1 = (unsigned)__float_as_int(tf.y) * 4u + tab_adj;
+  float S0, Q0, S1, Q1;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S0) : "r"(a0));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q0) : "r"(a0), "n"(4 * QMAX));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S1) : "r"(a1));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q1) : "r"(a1), "n"(4 * QMAX));
+  return fma2_(fr, make_float2(Q0, Q1), make_float2(S0, S1));
+}
+
+// Slices lane + 32 m: x += amp (H(upper) - H(lower)); the lower boundary of
+// slice lane + 32 m is the upper one of lane - 1 (lane 31 of step m - 1 for
+// lane 0).  FULL: every lane has ZPL slices and every boundary lies in the
+// table (steps evaluated in packed pairs); otherwise boundaries are clamped
+// to the table and slices >= nvalid dropped.
+template <int ZPL, bool FULL>
+__device__ __forceinline__ void b3_slices(float2 (&acc)[ZPL / 2], const B3Entry& e, int lane, int nvalid) {
+  constexpr int QMAX = B3Cfg<ZPL>::QMAX;
+  const float W0 = e.W0, B = e.B;
+  const float la1 = e.lxy * e.a1, la0 = e.lxy * e.a0, L2 = e.lxy * e.lxy;
+  // S table base minus 2^23 entries, read from the entry (an opaque value:
+  // the whole offset folds into one LEA per evaluation)
+  const unsigned tab_adj = (unsigned)e.pad;
+  const float wmax = (float)(4 * e.n4) - 0.5f;
+  const float lf = (float)lane;
+  // boundary w(i) = W0 + B i; this lane's upper boundaries i = lane + 1 + 32 m
+  const float wl = fmaf(B, lf + 1.0f, W0), B32 = 32.0f * B;
+  const float ql = fmaf(la1, lf, la0), la32 = 32.0f * la1;  // amp numerator at slice lane
+  const int src = (lane + 31) & 31;
+  if (FULL) {
+    const float Hlo0 = b3_eval<QMAX>(tab_adj, fmaf(B, lf, W0));
+    float rot_prev = 0.0f;
+    static_assert(ZPL % 2 == 0, "pairs of steps");
+#pragma unroll
+    for (int m = 0; m < ZPL; m += 2) {
+      const float2 w = make_float2(fmaf(B32, (float)m, wl), fmaf(B32, (float)(m + 1), wl));
+      const float2 Hu = b3_eval2<QMAX>(tab_adj, w);
+      const float r0 = __shfl_sync(0xffffffffu, Hu.x, src);
+      const float r1 = __shfl_sync(0xffffffffu, Hu.y, src);
+      const float2 Hl = make_float2(m == 0 ? Hlo0 : (lane == 0 ? rot_prev : r0), lane == 0 ? r0 : r1);
+      rot_prev = r1;
+      const float2 q = make_float2(fmaf(la32, (float)m, ql), fmaf(la32, (float)(m + 1), ql));
+      const float2 t = fma2_(q, q, bc2_(L2));
+      const float2 amp = make_float2(sqrt_approx(t.x), sqrt_approx(t.y));
+      acc[m / 2] = fma2_(amp, sub2_(Hu, Hl), acc[m / 2]);
+    }
+    return;
+  }
+  auto H = [&](float w) { return b3_eval<QMAX>(tab_adj, fminf(fmaxf(w, 0.0f), wmax)); };
+  const float Hlo0 = H(fmaf(B, lf, W0));
+  float rot_prev = 0.0f;
+#pragma unroll
+  for (int m = 0; m < ZPL; ++m) {
+    const float Hu = H(fmaf(B32, (float)m, wl));
+    const float rot = __shfl_sync(0xffffffffu, Hu, src);
+    const float Hl = m == 0 ? Hlo0 : (lane == 0 ? rot_prev : rot);
+    rot_prev = rot;
+    const float qa = fmaf(la32, (float)m, ql);
+    const float amp = sqrt_approx(fmaf(qa, qa, L2));
+    float& am = (m & 1) ? acc[m / 2].y : acc[m / 2].x;
+    if (m < nvalid) am = fmaf(amp, Hu - Hl, am);
+  }
+}
+
+// Direct path (wide footprints, split halves, long tables): rows r0 .. r0+K-1
+// of one slice, any footprint width, rows off the detector skipped.
+__device__ CTP_B3_RARE float b3_voxel_direct(float acc, float amp, float lo, float hi, const B3Entry& e,
+                                              const Trap& wide, int K, const float* __restrict__ yv, int nr,
+                                              int origin) {
+  const float fl = row_floor(lo);  // r0 - 1 (rows relative to origin)
+  const int r0 = (int)fl + 1 + origin;
+  float g = clampf_(add_(fl, 0.5f), lo, hi);
+  for (int k = 0; k < K; ++k) {
+    const int r = r0 + k;
+    const float gn = clampf_(add_(fl, (float)k + 1.5f), lo, hi);
+    float q = 0.0f;
+    if (r >= 0 && r < nr) {
+      if (e.ncol <= B3_NCF) {
+        for (int c = 0; c < e.ncol; ++c) q = fma_(e.ts[c], __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+      } else {
+        float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
+        for (int c = 0; c < e.ncol; ++c) {
+          const float cur = trap_cum(wide, add_((float)(e.cl + c), 0.5f));
+          q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+          prev = cur;
+        }
+      }
+    }
+    acc = fma_(mul_(amp, sub_(gn, g)), q, acc);
+    g = gn;
+  }
+  return acc;
+}
+
+template <int ZPL, bool VEC, bool FULL>
+__global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
+    const float* __restrict__ yT, float* __restrict__ out, int accumulate, int z0, int z1) {
+  using Cfg = B3Cfg<ZPL>;
+  extern __shared__ __align__(16) unsigned char b3_smem_raw[];
+  B3Smem<ZPL>& SM = *reinterpret_cast<B3Smem<ZPL>*>(b3_smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ix = blockIdx.x % gp.nx;
+  const int iy = (blockIdx.x / gp.nx) * B3_WARPS + warp;
+  if (iy >= gp.ny) return;  // warp-uniform; no CTA barriers below
+  const int b = blockIdx.z;
+  const int izs = z0 + blockIdx.y * Cfg::ZC;  // slices [z0, z1) of this launch
+  const int ize = min(izs + Cfg::ZC, z1) - 1;
+  const int nr = gp.nr;
+  const size_t view_elems = (size_t)gp.nc * nr;
+  const float* yb = yT + (size_t)b * gp.nv * view_elems;
+  float* tab = SM.tab[warp][0];
+  // table base minus 2^23 entries (b3_eval indexes it with the float bits)
+  const unsigned tab_adj = (unsigned)__cvta_generic_to_shared(tab) - 0x4B000000u * 4u;
+  B3Entry(&my)[32] = SM.ents[warp];
+  B3Entry& sp = SM.split[warp];
+  const int span = ize - izs;  // this lane's slices: izs + lane + 32 m, m < nvalid
+  const int nvalid = lane > span ? 0 : min(ZPL, (span - lane) / 32 + 1);
+  float2 acc[ZPL / 2];  // slices lane + 32 m: acc[m / 2].x (m even) / .y (m odd)
+#pragma unroll
+  for (int m = 0; m < ZPL / 2; ++m) acc[m] = make_float2(0.0f, 0.0f);
+
+  for (int vb = 0; vb < gp.nv; vb += 32) {
+    const int nsub = b3_setup<ZPL>(gp, vcoef, vax, vb, ix, iy, izs, ize, &my[lane], tab_adj) ? 2 : 1;
+    __syncwarp();
+    const int nvb = min(32, gp.nv - vb);
+    const float* yview = yb + (size_t)vb * view_elems;  // [c][r] of view vb + j
+    for (int j = 0; j < nvb; ++j, yview += view_elems) {
+#pragma unroll 1
+      for (int s = 0; s < nsub; ++s) {
+        if (s == 1) {
+          if (!(my[j].mask & 2)) continue;
+          __syncwarp();  // every lane is done with the previous split entry
+          if (lane == 0) b3_split<ZPL>(gp, vcoef, vax, vb + j, ix, iy, izs, ize, &sp, tab_adj);
+          __syncwarp();
+        }
+        const B3Entry& e = s == 0 ? my[j] : sp;
+        const int ncol = e.ncol;
+        if (ncol == 0) continue;
+        if (e.n4 > 0) {
+          const float* yc = yview + (size_t)e.cl * nr;
+          float ts[B3_NCF];
+#pragma unroll
+          for (int k = 0; k < B3_NCF; ++k) ts[k] = e.ts[k];
+          constexpr int NCH = (Cfg::QMAX + 255) / 256;
+          if (VEC && e.R0 >= 0 && e.R0 + 4 * e.n4 <= nr) {
+            const float* yr = yc + e.R0;
+            const int nq = 4 * e.n4;
+            switch (ncol) {  // warp-uniform: load only the footprint's columns
+              case 1: b3_table_fast<1, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+              case 2: b3_table_fast<2, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+              case 3: b3_table_fast<3, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+              default: b3_table_fast<4, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+            }
+          } else {
+            switch (ncol) {
+              case 1: b3_table_generic<1, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+              case 2: b3_table_generic<2, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+              case 3: b3_table_generic<3, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+              default: b3_table_generic<4, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+            }
+          }
+          __syncwarp();
+          b3_slices<ZPL, FULL>(acc, e, lane, nvalid);
+          __syncwarp();
+          continue;
+        }
+        // direct path
+        Trap wide{};
+        if (ncol > B3_NCF) {  // rare: rebuild the breakpoints of this footprint
+          SubFoot f0, f1;
+          column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
+          wide = make_trap(s == 0 ? f0 : f1);
+        }
+        const int K = rows_per_slice(e.B);
+        const float E = 0.5f * e.B;
+#pragma unroll
+        for (int m = 0; m < ZPL; ++m) {  // (unrolled: acc stays in registers)
+          if (m >= nvalid) break;
+          const float izf = (float)(lane + 32 * m);
+          const float T = fma_(e.B, izf, e.A);
+          const float lo = sub_(T, E), hi = add_(T, E);
+          const float q = fma_(e.a1, izf, e.a0);
+          const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+          float& am = (m & 1) ? acc[m / 2].y : acc[m / 2].x;
+          am = b3_voxel_direct(am, amp, lo, hi, e, wide, K, yview, nr, e.R0);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // out[b][iz][iy][ix]
+  const size_t plane = (size_t)gp.ny * gp.nx;
+  float* ob = out + (size_t)b * plane * gp.nz + (size_t)iy * gp.nx + ix;
+#pragma unroll
+  for (int m = 0; m < ZPL; ++m) {
+    if (m >= nvalid) break;
+    float* p = ob + (size_t)(izs + lane + 32 * m) * plane;
+    const float am = (m & 1) ? acc[m / 2].y : acc[m / 2].x;
+    *p = accumulate ? (*p + am) : am;
+  }
+}
+
+// FULL z-blocks (every lane has ZPL slices) and the partial last one are
+// separate instantiations, so the full blocks' slice loop has no clamps.
+template <int ZPL, bool VEC, bool FULL>
+static cudaError_t launch_back3d_t(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax,
+                                   const float* yT, float* vol, int batch, bool accumulate, cudaStream_t st,
+                                   int z0, int z1) {
+  auto kern = sf_back3d_kernel<ZPL, VEC, FULL>;
+  const int smem = (int)sizeof(B3Smem<ZPL>);
+  cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (ea != cudaSuccess) return ea;
+  const int nby = (gp.ny + B3_WARPS - 1) / B3_WARPS;
+  const size_t sino_elems = (size_t)gp.nv * gp.nr * gp.nc;
+  const size_t vol_elems = (size_t)gp.nx * gp.ny * gp.nz;
+  for (int b0 = 0; b0 < batch; b0 += 65535) {
+    const int nb = min(65535, batch - b0);
+    const dim3 grid(gp.nx * nby, (z1 - z0 + B3Cfg<ZPL>::ZC - 1) / B3Cfg<ZPL>::ZC, nb);
+    kern<<<grid, B3_WARPS * 32, smem, st>>>(gp, vcoef, vax, yT + (size_t)b0 * sino_elems,
+                                            vol + (size_t)b0 * vol_elems, accumulate ? 1 : 0, z0, z1);
+  }
+  return cudaGetLastError();
+}
+
+template <int ZPL, bool VEC>
+static cudaError_t launch_back3d_z(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax,
+                                   const float* yT, float* vol, int batch, bool accumulate, cudaStream_t st,
+                                   int z0, int z1) {
+  constexpr int ZC = B3Cfg<ZPL>::ZC;
+  const int zf = z0 + (z1 - z0) / ZC * ZC;  // end of the full z-blocks
+  cudaError_t e = cudaSuccess;
+  if (zf > z0) e = launch_back3d_t<ZPL, VEC, true>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, zf);
+  if (e == cudaSuccess && z1 > zf)
+    e = launch_back3d_t<ZPL, VEC, false>(gp, vcoef, vax, yT, vol, batch, accumulate, st, zf, z1);
+  return e;
+}
+
+cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
+                        float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
+  if (z1 < 0) z1 = gp.nz;
+  if (z0 < 0 || z0 >= z1 || z1 > gp.nz) return cudaErrorInvalidValue;
+  // the integral kernel below is not yet faster than round 1's per-row kernel
+  // on C3 (175 vs 166 ms); the latter stays the default until it is
+  static const bool integral = getenv("CTP_BACK_INTEGRAL") != nullptr;
+  if (!integral) return launch_back_legacy(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+  const bool vec = gp.nr % 4 == 0 && (reinterpret_cast<uintptr_t>(yT) & 15) == 0;
+  static const int zpl_env = getenv("CTP_B3_ZPL") ? atoi(getenv("CTP_B3_ZPL")) : 16;  // (tuning)
+  // tall z-ranges: 512 slices per warp (16 per lane); short ones: 128
+  if (zpl_env == 8 && z1 - z0 >= 192)
+    return vec ? launch_back3d_z<8, true>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1)
+               : launch_back3d_z<8, false>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+  if (z1 - z0 >= 384)
+    return vec ? launch_back3d_z<16, true>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1)
+               : launch_back3d_z<16, false>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+  return vec ? launch_back3d_z<4, true>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1)
+             : launch_back3d_z<4, false>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+}
+
+}  // namespace ctp

@@ -197,6 +197,21 @@ __device__ __forceinline__ float col_weight(const Trap& p, int col) {
   return sub_(trap_cum(p, add_(c, 0.5f)), trap_cum(p, sub_(c, 0.5f)));
 }
 
+// Column weights of NW consecutive detector columns c_first.. : NW+1 shared
+// boundary evaluations of the trapezoid integral.  ts(c) = F(c+.5) - F(c-.5)
+// with exactly the same F values wherever a boundary is shared, so any caller
+// (back: footprint columns, forward: tile columns) gets bitwise equal weights.
+template <int NW>
+__device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&ts)[NW]) {
+  float prev = trap_cum(p, sub_((float)c_first, 0.5f));
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const float cur = trap_cum(p, add_((float)(c_first + k), 0.5f));
+    ts[k] = sub_(cur, prev);
+    prev = cur;
+  }
+}
+
 // Axial map (_kernels.py:619-645) in row units: slice iz spans
 // [T - E, T + E] with T = A + B iz; its weight in row r is the overlap with
 // [r - 0.5, r + 0.5] written as a difference of clamped boundaries,
@@ -378,6 +393,58 @@ __device__ __forceinline__ void axial64(const ViewAx& a, int kind, double X, dou
   }
   A = fma(mag, fma(a.a3, Y, fma(a.a2, X, a.a1)), a.a0);
   B = mag * a.bz;
+}
+
+// ---- forward-kernel helpers shared by the 3D and fan forward kernels ----
+// boundary ray of the tile edge at column coordinate S (centred grid-index coords)
+__device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& gp, float S,
+                                         float& px, float& py, float& dx, float& dy) {
+  const float s_mm = (S - gp.cc) * gp.pw;  // transverse detector coordinate (mm)
+  if (gp.kind == kConeCurved) {
+    const float th = s_mm / gp.sdd;
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    px = vc.xs; py = vc.ys;
+    dx = cs * vc.wx + sn * vc.ux;
+    dy = cs * vc.wy + sn * vc.uy;
+    return;
+  }
+  if (gp.kind == kModular) {
+    // line {S(X, Y) = S} at the reference height: g num - (S - s0) den = 0
+    const float kk = S - vc.s0;
+    const float al = vc.g * vc.nb - kk * vc.db, be = vc.g * vc.nc - kk * vc.dc;
+    const float ga = vc.g * vc.na - kk * vc.da;
+    const float n2 = al * al + be * be;
+    px = -ga * al / n2;
+    py = -ga * be / n2;
+    dx = be;
+    dy = -al;
+    return;
+  }
+  const float k = s_mm / gp.hx;
+  px = vc.xc0 + k * vc.ux;
+  py = vc.yc0 + k * vc.uy;
+  if (gp.kind == kParallel) {
+    dx = vc.wx; dy = vc.wy;
+  } else {
+    dx = px - vc.xs; dy = py - vc.ys;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += n;
+  }
+  return v;
 }
 
 #endif  // __CUDACC__

@@ -1,0 +1,538 @@
+// sf_forward3d.cu -- 3D forward projection y = A x of the SF-TR pair
+// (parallel, cone flat/curved, SF-modular), ray-driven GATHER (reference:
+// sf_forward_kernel -> _sf_view_accumulate, _kernels.py:555-663).
+//
+// Integral formulation.  For one voxel column in one view the axial
+// footprints of consecutive slices tile the detector column: slice j spans
+// rows [Lo + B j, Lo + B (j + 1)) (row units, B = mag hz / ph), so the
+// column's contribution to detector row r is
+//
+//   P(r) = sum_j overlap(slice j, row r) amp_j x_j = B (Fn(u(r + 1/2)) - Fn(u(r - 1/2))),
+//   u(t) = (t - Lo) / B,   Fn(u) = G_k + (u - k) xa_k,   k = floor(u),
+//
+// with xa_j = amp_j x_j and G_k = sum_{i<k} xa_i.  The reference sums the
+// 2-3 overlapping slices of each row (_kernels.py:619-647); here the warp
+// stages (G, xa) of the column's slices once per task (warp prefix scan),
+// and every row costs ONE table evaluation: lane l owns row 32 k + l of the
+// band, evaluates Fn at the row's upper boundary and takes the lower one from
+// lane l - 1 with a shuffle.  y(r, c) += (B ts(c)) (Fn_up - Fn_lo).
+//
+// Task decomposition, wedge enumeration and candidate setup follow round 1:
+// one WARP owns (view, F3_CW-column tile, F3_KR * 32-row band); it enumerates
+// the wedge of voxel columns between the tile's edge rays, sets the
+// candidates up lane-parallel (transverse weights in fp32, axial map in f64 at
+// the (sub-)voxel centre, relative to the band), and gathers them into its
+// register tile.  The next entry's x column is prefetched with cp.async while
+// the current one is processed.  No atomics, no CTA barriers.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "sf_common.cuh"
+#include "sf_launch.h"
+
+#ifndef CTP_F3_MINB
+#define CTP_F3_MINB 3
+#endif
+#ifndef CTP_F3_KR
+#define CTP_F3_KR 24
+#endif
+
+namespace ctp {
+
+constexpr int F3_CW = 4;              // detector columns per tile
+constexpr int F3_KR = CTP_F3_KR;      // 32-row groups per warp task (24: a 768-row detector in one band)
+static_assert(F3_KR % 4 == 0, "row groups are processed in blocks of 4 (two packed pairs)");
+constexpr int F3_ROWS = 32 * F3_KR;   // rows per band
+constexpr int F3_VCH = 16;            // views per chunk of the task order
+constexpr int F3_WARPS = 4;           // independent warps per CTA
+constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
+constexpr int F3_XLEN = F3_XCAP + 4;  // + the total / zero pad entry
+constexpr int F3_EBUF = 96;           // >= 31 pending + 64 from one setup round
+static_assert(F3_KR <= 31, "row groups are 5-bit in F3Entry::info");
+
+struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
+  int col;        // x offset of the first staged slice za4 (float4 units on the vector path)
+  int info;       // g0 | g1 << 5 | fast << 10 | nst << 11 (nst staged slices; 0: misses the band)
+  float cu;       // u(r + 1/2) = r invB + cu: upper boundary of band row r in staged-slice units
+  float invB;     // 1 / rows per slice
+  float lxy;      // amp(s) = lxy sqrt(1 + (a0 + a1 s)^2), s = staged slice index
+  float a0, a1;
+  unsigned gadj;   // the warp's G table base - 2^23 entries (shared address; opaque, see f3_eval)
+  float bts[F3_CW];  // B * ts(c) of the tile's columns (0 outside the footprint)
+};
+static_assert(sizeof(F3Entry) == 48, "F3Entry layout");
+
+struct F3Smem {  // per warp
+  F3Entry ent[F3_EBUF];
+  float G[F3_XLEN];          // exclusive prefix of amp * x over the staged slices; G[n] = total
+  float X[F3_XLEN];          // amp * x; X[n] = 0
+  float xr[2][F3_XCAP];      // raw x of the next fast entries (cp.async)
+};
+
+__device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// Candidate entry for this task: transverse weights of the tile's columns
+// (fp32, sf_common.cuh) and the band-relative axial map in f64 at the
+// (sub-)voxel centre.  Returns false if the (sub-)voxel misses the tile or
+// the band.
+__device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const GridParams& gp, int col, int c0, int cw,
+                                        const ViewAx& ax, float2 cxy, int rw0, int nrows, bool vec) {
+  if (max(f.cl, c0) > min(f.ch, c0 + cw - 1)) return false;
+  double A, B;
+  axial64(ax, gp.kind, (double)cxy.x, (double)cxy.y, A, B);
+  A -= (double)rw0;  // row coordinate of slice 0's centre, band-relative
+  // rows the column reaches (row r spans [r - .5, r + .5))
+  const double top = A + B * ((double)gp.nz - 0.5);
+  const double bot = A - 0.5 * B;
+  const double rl = floor(bot + 0.5), rh = floor(top + 0.5);
+  if (rh < 0.0 || rl > (double)(nrows - 1)) return false;
+  const int r_lo = rl < 0.0 ? 0 : (int)rl, r_hi = rh > (double)(nrows - 1) ? nrows - 1 : (int)rh;
+  // slices reaching band rows [0, nrows): one slice of slack on each side
+  const double invB = 1.0 / B;
+  int za = (int)floor((-0.5 - A) * invB - 0.5);
+  int zb = (int)ceil(((double)nrows - 0.5 - A) * invB + 0.5);
+  za = max(za, 0);
+  zb = min(zb, gp.nz - 1);
+  if (za > zb) return false;
+  const int za4 = vec ? (za & ~3) : za;
+  const int nst = zb - za4 + 1;
+  const double Lo = A + B * ((double)za4 - 0.5);  // lower boundary of staged slice 0
+  e.cu = (float)((0.5 - Lo) * invB);
+  e.invB = (float)invB;
+  e.lxy = f.lxy;
+  e.a1 = f.a1;
+  e.a0 = fma_(f.a1, (float)za4, f.a0);
+  const Trap p = make_trap(f);
+  float ts[F3_CW];
+  col_weights<F3_CW>(p, c0, ts);
+  const int lo = max(f.cl, c0), hi = min(f.ch, c0 + cw - 1);
+  const float Bf = (float)B;
+#pragma unroll
+  for (int c = 0; c < F3_CW; ++c) e.bts[c] = (c0 + c >= lo && c0 + c <= hi) ? Bf * ts[c] : 0.0f;
+  // x offset of slice za4 (32-bit: the launcher checks nx*ny*nz < 2^34 resp. 2^32)
+  const unsigned xo = (unsigned)(((unsigned long long)(unsigned)col * (unsigned)gp.nz + (unsigned)za4) >> (vec ? 2 : 0));
+  e.col = (int)xo;
+  const int g0 = r_lo >> 5, g1 = r_hi >> 5;
+  const bool fast = nst <= F3_XCAP;
+  e.info = g0 | (g1 << 5) | (fast ? (1 << 10) : 0) | (nst << 11);
+  return true;
+}
+
+// Lane-parallel setup of wedge candidates k = cbase + lane: owner primary
+// index by binary search over the exclusive scan, footprint of the voxel
+// column, compaction of the (sub-)footprints that reach the tile and band.
+// Returns how many entries the warp added.  Out of line (its registers stay
+// out of the gather loop).
+__device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp,
+                                          const ViewAx* __restrict__ vaxp, F3Entry* ent, int k, int total, int ib,
+                                          int excl, int jl, bool primary_x, int c0, int cw, int rw0, int nrows,
+                                          bool vec, unsigned gadj) {
+  const int lane = threadIdx.x & 31;
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int ex = __shfl_sync(0xffffffffu, excl, o + step);
+    if (ex <= k) o += step;
+  }
+  const int jo = __shfl_sync(0xffffffffu, jl, o);
+  const int exo = __shfl_sync(0xffffffffu, excl, o);
+  F3Entry e0, e1;
+  int mask = 0;
+  if (k < total) {
+    const ViewCoef vc = *vcp;
+    const ViewAx ax = *vaxp;
+    const int ii = ib + o, j = jo + (k - exo);
+    const int ix = primary_x ? ii : j, iy = primary_x ? j : ii;
+    const int col = iy * gp.nx + ix;
+    SubFoot f0, f1;
+    float2 cxy0, cxy1;
+    const int m = column_subs(vc, gp, ix, iy, f0, f1, cxy0, cxy1) & 3;
+    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, vec)) mask |= 1;
+    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, vec)) mask |= 2;
+  }
+  const int n = __popc(mask);
+  const int ni = warp_incl_scan(n, lane);
+  const int off = ni - n;
+  e0.gadj = e1.gadj = gadj;
+  if (mask & 1) ent[off] = e0;
+  if (mask & 2) ent[off + (mask & 1)] = e1;
+  return __shfl_sync(0xffffffffu, ni, 31);
+}
+
+// Stage (G, X) of n <= F3_XCAP slices: lane t takes slices 256 c + 4 t .. + 3
+// and 256 c + 128 + 4 t .. + 3 of chunk c (512 contiguous bytes per 16-byte
+// access), amp * x, local prefixes and two warp scans per chunk; G[n] ends up
+// as the exclusive prefix at n (the total).
+//   RAW (x in the cp.async buffer xraw, finite everywhere): slices >= n are
+//   staged like the others -- they only change G / X past index n, which no
+//   evaluation reads (u <= n, and at u = n the weight of X[n] is exactly 0).
+//   Otherwise (global x): slices >= n read as 0 and X[n] = 0.
+template <bool RAW, bool VEC>
+__device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const float* __restrict__ xg, int n, float a0,
+                                         float a1, float lxy, int lane) {
+  float carry = 0.0f;
+#pragma unroll
+  for (int c = 0; c < F3_XCAP / 256; ++c) {
+    if (256 * c >= n) break;  // warp-uniform
+    float2 xa[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s = 256 * c + 128 * h + 4 * lane;
+      float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (RAW) {
+        v = *reinterpret_cast<const float4*>(xraw + s);
+      } else if (s < n) {
+        if (VEC) {
+          v = __ldg(reinterpret_cast<const float4*>(xg + s));
+        } else {
+          v.x = __ldg(xg + s);
+          if (s + 1 < n) v.y = __ldg(xg + s + 1);
+          if (s + 2 < n) v.z = __ldg(xg + s + 2);
+          if (s + 3 < n) v.w = __ldg(xg + s + 3);
+        }
+        if (s + 3 >= n) {  // slices past the staged range add nothing
+          if (s + 1 >= n) v.y = 0.0f;
+          if (s + 2 >= n) v.z = 0.0f;
+          v.w = 0.0f;
+        }
+      }
+      const float sf = (float)s;
+      const float2 iA = make_float2(sf, sf + 1.0f), iB = make_float2(sf + 2.0f, sf + 3.0f);
+      const float2 qA = fma2_(bc2_(a1), iA, bc2_(a0)), qB = fma2_(bc2_(a1), iB, bc2_(a0));
+      const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
+      const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
+      const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
+      xa[2 * h] = mul2_(ampA, make_float2(v.x, v.y));
+      xa[2 * h + 1] = mul2_(ampB, make_float2(v.z, v.w));
+    }
+    const float a_1 = xa[0].x, a_2 = a_1 + xa[0].y, a_3 = a_2 + xa[1].x, ta = a_3 + xa[1].y;
+    const float b_1 = xa[2].x, b_2 = b_1 + xa[2].y, b_3 = b_2 + xa[3].x, tb = b_3 + xa[3].y;
+    float ia = ta, ib = tb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float na = __shfl_up_sync(0xffffffffu, ia, d);
+      const float nb = __shfl_up_sync(0xffffffffu, ib, d);
+      if (lane >= d) {
+        ia += na;
+        ib += nb;
+      }
+    }
+    const float tot_a = __shfl_sync(0xffffffffu, ia, 31);
+    const float tot_b = __shfl_sync(0xffffffffu, ib, 31);
+    const float ea = carry + (ia - ta), eb = (carry + tot_a) + (ib - tb);
+    const float2 e01 = add2_(bc2_(ea), make_float2(0.0f, a_1)), e23 = add2_(bc2_(ea), make_float2(a_2, a_3));
+    const float2 f01 = add2_(bc2_(eb), make_float2(0.0f, b_1)), f23 = add2_(bc2_(eb), make_float2(b_2, b_3));
+    const int s0 = 256 * c + 4 * lane, s1 = s0 + 128;
+    // RAW: the float4 that holds (or starts at) index n carries G[n]
+    if (RAW ? s0 <= n : s0 < n) {
+      *reinterpret_cast<float4*>(S.G + s0) = make_float4(e01.x, e01.y, e23.x, e23.y);
+      *reinterpret_cast<float4*>(S.X + s0) = make_float4(xa[0].x, xa[0].y, xa[1].x, xa[1].y);
+    }
+    if (RAW ? s1 <= n : s1 < n) {
+      *reinterpret_cast<float4*>(S.G + s1) = make_float4(f01.x, f01.y, f23.x, f23.y);
+      *reinterpret_cast<float4*>(S.X + s1) = make_float4(xa[2].x, xa[2].y, xa[3].x, xa[3].y);
+    }
+    carry += tot_a + tot_b;
+  }
+  // pad entry (u = n evaluates to the total) where no store above wrote it
+  if (!RAW || (n & 255) == 0) {
+    __syncwarp();
+    if (lane == 0) {
+      S.G[n] = carry;
+      S.X[n] = 0.0f;
+    }
+  }
+}
+
+// Fn(u) = G_k + (u - k) X_k, k = floor(u), 0 <= u <= n: floor by adding 2^23
+// with round-down and the index from the sum's bits (no conversion pipe).
+__device__ __forceinline__ float f3_eval(unsigned g_adj, float u) {
+  const float tf = __fadd_rd(u, 8388608.0f);
+  const float fr = u - (tf - 8388608.0f);  // both subtractions exact
+  const unsigned a = (unsigned)__float_as_int(tf) * 4u + g_adj;
+  float G, X;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X) : "r"(a), "n"(4 * F3_XLEN));
+  return fmaf(fr, X, G);
+}
+
+// Rows 32 k + lane of the groups g0..g1, in blocks of four groups (a block
+// outside [g0, g1] is skipped; inside one, every group is evaluated, rows
+// beyond the column's reach clamp u to [0, n] and add exactly 0) and packed
+// pairs of groups: acc(r, c) += bts(c) (Fn(u(r + .5)) - Fn(u(r - .5))).
+__device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
+  float2 tf;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\t"
+      "add.rm.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(tf.x), "=f"(tf.y) : "f"(u.x), "f"(u.y), "f"(8388608.0f));
+  const float2 fr = sub2f_(u, add2_(tf, bc2_(-8388608.0f)));  // exact
+  const unsigned a0 = (unsigned)__float_as_int(tf.x) * 4u + g_adj;
+  const unsigned a1 = (unsigned)__float_as_int(tf.y) * 4u + g_adj;
+  float G0, X0, G1, X1;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G0) : "r"(a0));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X0) : "r"(a0), "n"(4 * F3_XLEN));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G1) : "r"(a1));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X1) : "r"(a1), "n"(4 * F3_XLEN));
+  return fma2_(fr, make_float2(X0, X1), make_float2(G0, G1));
+}
+
+__device__ __forceinline__ void f3_rows(float (&acc)[F3_KR][F3_CW], unsigned g_adj, float cu, float invB,
+                                        const float (&bts)[F3_CW], int n, int g0, int g1, int lane) {
+  const float umax = (float)n;
+  const float uL = fmaf((float)lane, invB, cu), du = 32.0f * invB;
+  const int kb0 = g0 & ~3;
+  // lower boundary of the first evaluated group's rows (used by lane 0)
+  float rot_prev = f3_eval(g_adj, fminf(fmaxf(fmaf(du, (float)kb0, uL - invB), 0.0f), umax));
+  const int src = (lane + 31) & 31;
+  const bool l0 = lane == 0;
+  const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
+#pragma unroll
+  for (int kb = 0; kb < F3_KR; kb += 4) {
+    if (kb + 3 < g0 || kb > g1) continue;  // warp-uniform
+    // interior block: every boundary of its 128 rows lies in [0, n] (no clamps)
+    const bool inner = fmaf((float)(32 * kb - 1), invB, cu) >= 0.0f &&
+                       fmaf((float)(32 * kb + 127), invB, cu) <= umax;
+#pragma unroll
+    for (int k = kb; k < kb + 4; k += 2) {
+      float2 u = make_float2(fmaf(du, (float)k, uL), fmaf(du, (float)(k + 1), uL));
+      if (!inner) {
+        u.x = fminf(fmaxf(u.x, 0.0f), umax);
+        u.y = fminf(fmaxf(u.y, 0.0f), umax);
+      }
+      const float2 Fu = f3_eval2(g_adj, u);
+      const float r0 = __shfl_sync(0xffffffffu, Fu.x, src);
+      const float r1 = __shfl_sync(0xffffffffu, Fu.y, src);
+      const float2 d = sub2f_(Fu, make_float2(l0 ? rot_prev : r0, l0 ? r0 : r1));
+      rot_prev = r1;
+      float2 a;
+      a = fma2_(b01, bc2_(d.x), make_float2(acc[k][0], acc[k][1]));
+      acc[k][0] = a.x; acc[k][1] = a.y;
+      a = fma2_(b23, bc2_(d.x), make_float2(acc[k][2], acc[k][3]));
+      acc[k][2] = a.x; acc[k][3] = a.y;
+      a = fma2_(b01, bc2_(d.y), make_float2(acc[k + 1][0], acc[k + 1][1]));
+      acc[k + 1][0] = a.x; acc[k + 1][1] = a.y;
+      a = fma2_(b23, bc2_(d.y), make_float2(acc[k + 1][2], acc[k + 1][3]));
+      acc[k + 1][2] = a.x; acc[k + 1][3] = a.y;
+    }
+  }
+}
+
+template <bool VEC>
+__device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[F3_KR][F3_CW],
+                                           const float* __restrict__ xb, int lane) {
+  int pbuf = 0;  // xr buffer the next prefetch goes to
+  // x of the next fast entry is in flight (cp.async, 16-byte copies on the
+  // vector path) while the current one is processed
+  auto next_fast = [&](int e) {
+    for (; e < nent; ++e) {
+      const int info = S.ent[e].info;
+      if (info & (1 << 10)) {
+        if (VEC) {
+          const float* xc = xb + ((size_t)(unsigned)S.ent[e].col << 2);
+          const int nst = info >> 11;
+#pragma unroll
+          for (int t = 0; t < F3_XCAP / 128; ++t) {
+            const int s = 4 * lane + 128 * t;
+            if (s < nst) cp_async16(&S.xr[pbuf][s], xc + s);
+          }
+          cp_async_commit();
+          pbuf ^= 1;
+        }
+        return e;
+      }
+    }
+    return nent;
+  };
+  int e_pf = next_fast(0);
+  for (int e = 0; e < nent; ++e) {
+    const F3Entry& E = S.ent[e];
+    const int info = E.info;
+    const int nst = info >> 11;
+    if (nst == 0) continue;
+    const float cu = E.cu, invB = E.invB, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
+    const unsigned g_adj = E.gadj;
+    const int g0 = info & 31, g1 = (info >> 5) & 31;
+    float bts[F3_CW];
+#pragma unroll
+    for (int c = 0; c < F3_CW; ++c) bts[c] = E.bts[c];
+    const float* xg = xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0));
+    if (e == e_pf) {  // fast: one piece, x staged by cp.async (vector path)
+      const float* xraw = nullptr;
+      if (VEC) {
+        cp_async_wait_all();  // this lane's copies; the warp barrier publishes the others'
+        __syncwarp();
+        xraw = S.xr[pbuf ^ 1];
+      }
+      if (VEC) f3_stage<true, true>(S, xraw, xg, nst, a0, a1, lxy, lane);
+      else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lxy, lane);
+      __syncwarp();
+      e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
+      f3_rows(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      __syncwarp();
+      continue;
+    }
+    // generic: pieces of F3_XCAP slices; each piece's clamped differences add
+    // up to the whole column's (the integral is additive over pieces)
+    for (int p0 = 0; p0 < nst; p0 += F3_XCAP) {
+      const int n = min(F3_XCAP, nst - p0);
+      f3_stage<false, false>(S, nullptr, xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0)) + p0, n,
+                      fma_(a1, (float)p0, a0), a1, lxy, lane);
+      __syncwarp();
+      f3_rows(acc, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
+      __syncwarp();
+    }
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kernel(
+    const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
+    const float* __restrict__ xT, float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
+  extern __shared__ __align__(16) unsigned char f3_smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  F3Smem& S = reinterpret_cast<F3Smem*>(f3_smem_raw)[warp];
+  const long long task = task0 + (long long)blockIdx.x * F3_WARPS + warp;
+  if (task >= ntasks) return;  // warp-uniform; no CTA barriers in this kernel
+  const int ntiles = (gp.nc + F3_CW - 1) / F3_CW;
+  // band-major task order; within a band, chunks of F3_VCH consecutive views x
+  // all tiles, so the CTAs resident at once cover a few degrees of rotation
+  // whose wedges stay in L2
+  const long long per_band = (long long)ntiles * gp.nv * gp.batch;
+  const int band = (int)(task / per_band);
+  const long long t2 = task % per_band;
+  const int nvb = gp.nv * gp.batch;
+  const int vch = (int)(t2 / ((long long)ntiles * F3_VCH));
+  const int rem = (int)(t2 - (long long)vch * ntiles * F3_VCH);
+  const int cv = min(F3_VCH, nvb - vch * F3_VCH);
+  const int tile = rem / cv;
+  const int vb = vch * F3_VCH + rem % cv;
+  const int v = vb % gp.nv, b = vb / gp.nv;
+  const int c0 = tile * F3_CW;
+  const int cw = min(F3_CW, gp.nc - c0);
+  const int rw0 = band * F3_ROWS;
+  const int nrows = min(F3_ROWS, gp.nr - rw0);
+  const ViewCoef vc = vcoef[v];
+
+  // wedge between the tile's edge rays, in (primary, secondary) grid axes
+  float plx, ply, dlx, dly, phx, phy, dhx, dhy;
+  edge_ray(vc, gp, (float)c0 - 0.5f, plx, ply, dlx, dly);
+  edge_ray(vc, gp, (float)(c0 + cw) - 0.5f, phx, phy, dhx, dhy);
+  const float nl = rsqrtf(dlx * dlx + dly * dly), nh = rsqrtf(dhx * dhx + dhy * dhy);
+  const bool primary_x = fabsf(dlx) * nl + fabsf(dhx) * nh >= fabsf(dly) * nl + fabsf(dhy) * nh;
+  const int nP = primary_x ? gp.nx : gp.ny, nQ = primary_x ? gp.ny : gp.nx;
+  const float halfP = primary_x ? gp.half_x : gp.half_y, halfQ = primary_x ? gp.half_y : gp.half_x;
+  const float lp = primary_x ? plx : ply, lq = primary_x ? ply : plx;
+  const float ldp = primary_x ? dlx : dly, ldq = primary_x ? dly : dlx;
+  const float hp = primary_x ? phx : phy, hq = primary_x ? phy : phx;
+  const float hdp = primary_x ? dhx : dhy, hdq = primary_x ? dhy : dhx;
+  const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
+  const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
+
+  float acc[F3_KR][F3_CW];
+#pragma unroll
+  for (int k = 0; k < F3_KR; ++k)
+#pragma unroll
+    for (int c = 0; c < F3_CW; ++c) acc[k][c] = 0.0f;
+  const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
+  if (VEC) {  // the RAW staging reads the cp.async buffers past nst: keep them finite
+    for (int i = lane; i < 2 * F3_XCAP; i += 32) (&S.xr[0][0])[i] = 0.0f;
+    __syncwarp();
+  }
+  const unsigned g_adj = (unsigned)__cvta_generic_to_shared(S.G) - 0x4B000000u * 4u;
+
+  int pending = 0;
+  for (int ib = 0; ib < nP; ib += 32) {
+    // secondary-index range of primary index i on the two edge rays (+-1 margin)
+    const int i = ib + lane;
+    int jl = 0, cnt = 0;
+    if (i < nP) {
+      int jh = nQ - 1;
+      if (cull) {
+        const float pa = (float)i - halfP, pb = pa + 1.0f;
+        const float q0 = lq + (pa - lp) * lslope, q1 = lq + (pb - lp) * lslope;
+        const float q2 = hq + (pa - hp) * hslope, q3 = hq + (pb - hp) * hslope;
+        const float qmin = fminf(fminf(q0, q1), fminf(q2, q3)) + halfQ;
+        const float qmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) + halfQ;
+        if (qmin > -1e8f && qmax < 1e8f) {
+          jl = max(jl, (int)floorf(qmin) - 1);
+          jh = min(jh, (int)floorf(qmax) + 1);
+        }
+      }
+      cnt = jh >= jl ? jh - jl + 1 : 0;
+    }
+    const int incl = warp_incl_scan(cnt, lane);
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int cbase = 0; cbase < total; cbase += 32) {
+      pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
+                               primary_x, c0, cw, rw0, nrows, VEC, g_adj);
+      __syncwarp();
+      if (pending >= 32) {
+        f3_process<VEC>(S, pending, acc, xb, lane);
+        pending = 0;
+        __syncwarp();
+      }
+    }
+  }
+  if (pending > 0) f3_process<VEC>(S, pending, acc, xb, lane);
+
+  // store the tile: y[b][v][r][c0 + c], rows rw0 + 32 k + lane
+  float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
+  const bool v4 = cw == F3_CW && (gp.nc & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+#pragma unroll
+  for (int k = 0; k < F3_KR; ++k) {
+    const int r = 32 * k + lane;
+    if (r >= nrows) continue;
+    float* row = yv + (size_t)(rw0 + r) * gp.nc + c0;
+    if (v4) {
+      float4 o = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
+      if (accumulate) {
+        const float4 p = *reinterpret_cast<const float4*>(row);
+        o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+      }
+      *reinterpret_cast<float4*>(row) = o;
+    } else {
+#pragma unroll
+      for (int c = 0; c < F3_CW; ++c) {
+        if (c >= cw) break;
+        row[c] = accumulate ? row[c] + acc[k][c] : acc[k][c];
+      }
+    }
+  }
+}
+
+cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                           float* sino, int batch, bool accumulate, cudaStream_t st) {
+  static const bool legacy = getenv("CTP_FWD_LEGACY") != nullptr;  // A/B against round 1's kernel
+  if (legacy) return launch_forward_legacy(gp, vcoef, vax, xT, sino, batch, accumulate, st);
+  const size_t smem = sizeof(F3Smem) * F3_WARPS;
+  // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
+  const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
+  if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
+  auto kern = vec ? sf_forward3d_kernel<true> : sf_forward3d_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long nbands = (gp.nr + F3_ROWS - 1) / F3_ROWS;
+  const long long ntiles = (gp.nc + F3_CW - 1) / F3_CW;
+  const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
+  const long long max_blocks = 1LL << 30;
+  GridParams g2 = gp;
+  g2.batch = batch;  // the task decode needs the batch extent
+  for (long long t0 = 0; t0 < ntasks; t0 += max_blocks * F3_WARPS) {
+    const long long rem = ntasks - t0;
+    const long long nb = (rem + F3_WARPS - 1) / F3_WARPS;
+    const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
+    kern<<<grid, F3_WARPS * 32, smem, st>>>(g2, vcoef, vax, xT, sino, accumulate ? 1 : 0, t0, ntasks);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ctp

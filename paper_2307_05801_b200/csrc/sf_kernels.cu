@@ -62,21 +62,6 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
   }
 }
 
-// Column weights of NW consecutive detector columns c_first.. : NW+1 shared
-// boundary evaluations of the trapezoid integral.  ts(c) = F(c+.5) - F(c-.5)
-// with exactly the same F values wherever a boundary is shared, so any caller
-// (back: footprint columns, forward: tile columns) gets bitwise equal weights.
-template <int NW>
-__device__ __forceinline__ void col_weights(const Trap& p, int c_first, float (&ts)[NW]) {
-  float prev = trap_cum(p, sub_((float)c_first, 0.5f));
-#pragma unroll
-  for (int k = 0; k < NW; ++k) {
-    const float cur = trap_cum(p, add_((float)(c_first + k), 0.5f));
-    ts[k] = sub_(cur, prev);
-    prev = cur;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // back projection: x = A^T y
 // ---------------------------------------------------------------------------
@@ -805,41 +790,6 @@ __device__ __forceinline__ void fw_rows(float (&acc)[FW_KR][FW_CW], const float 
   }
 }
 
-// boundary ray of the tile edge at column coordinate S (centred grid-index coords)
-__device__ __forceinline__ void edge_ray(const ViewCoef& vc, const GridParams& gp, float S,
-                                         float& px, float& py, float& dx, float& dy) {
-  const float s_mm = (S - gp.cc) * gp.pw;  // transverse detector coordinate (mm)
-  if (gp.kind == kConeCurved) {
-    const float th = s_mm / gp.sdd;
-    float sn, cs;
-    sincosf(th, &sn, &cs);
-    px = vc.xs; py = vc.ys;
-    dx = cs * vc.wx + sn * vc.ux;
-    dy = cs * vc.wy + sn * vc.uy;
-    return;
-  }
-  if (gp.kind == kModular) {
-    // line {S(X, Y) = S} at the reference height: g num - (S - s0) den = 0
-    const float kk = S - vc.s0;
-    const float al = vc.g * vc.nb - kk * vc.db, be = vc.g * vc.nc - kk * vc.dc;
-    const float ga = vc.g * vc.na - kk * vc.da;
-    const float n2 = al * al + be * be;
-    px = -ga * al / n2;
-    py = -ga * be / n2;
-    dx = be;
-    dy = -al;
-    return;
-  }
-  const float k = s_mm / gp.hx;
-  px = vc.xc0 + k * vc.ux;
-  py = vc.yc0 + k * vc.uy;
-  if (gp.kind == kParallel) {
-    dx = vc.wx; dy = vc.wy;
-  } else {
-    dx = px - vc.xs; dy = py - vc.ys;
-  }
-}
-
 // ---- warp-independent forward ------------------------------------------------
 // One WARP owns one task = (view, FW_CW-column tile, FW_KR*32-row band).  It
 // enumerates the wedge of voxel columns reaching its tile (rows of primary
@@ -865,23 +815,7 @@ struct FvSmem {
 #endif
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
 size_t forward_warp_smem_bytes() { return sizeof(FvSmem) * FV_WARPS; }
-
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int n = __shfl_up_sync(0xffffffffu, v, d);
-    if (lane >= d) v += n;
-  }
-  return v;
-}
 
 // issue the loads of x for the staged slices of one entry (16-byte loads when
 // the column layout allows, slots >= nst read as 0)
@@ -1550,8 +1484,8 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
   return cudaGetLastError();
 }
 
-cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
-                        float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
+cudaError_t launch_back_legacy(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
+                               float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
   if (z1 < 0) z1 = gp.nz;
   if (z0 < 0 || z0 >= z1 || z1 > gp.nz) return cudaErrorInvalidValue;
   cudaError_t ea = cudaFuncSetAttribute(sf_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1570,8 +1504,8 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewA
   return cudaGetLastError();
 }
 
-cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
-                           float* sino, int batch, bool accumulate, cudaStream_t st) {
+cudaError_t launch_forward_legacy(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                                  float* sino, int batch, bool accumulate, cudaStream_t st) {
   const size_t smem = forward_warp_smem_bytes();
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;

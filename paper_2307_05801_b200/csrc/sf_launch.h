@@ -21,6 +21,12 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const Vi
 constexpr int kBackZBlock = 256;  // slices per back-kernel z-block (BK_ZC)
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
                         float* vol, int batch, bool accumulate, cudaStream_t st, int z0 = 0, int z1 = -1);
+// round-1 3D back kernel (per-row overlaps), kept for A/B measurements
+cudaError_t launch_back_legacy(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
+                               float* vol, int batch, bool accumulate, cudaStream_t st, int z0 = 0, int z1 = -1);
+// round-1 3D forward kernel (per-row candidate overlaps), kept for A/B measurements
+cudaError_t launch_forward_legacy(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                                  float* sino, int batch, bool accumulate, cudaStream_t st);
 size_t forward_warp_smem_bytes();
 // fan beam (nz == nr == 1) with the batch on the lanes: inputs batch-innermost
 // (xB [ny*nx][batch], yB [nv][nc][batch]), outputs in the natural layouts

@@ -438,7 +438,8 @@ def test_zslab_parallel_partition_on_device(world, oracle_mod):
 def test_full_size_adjoint_and_linearity(which):
     """Whole C3 (512^3 x 720, 768^2) and C5 (1024^3 x 1440, 1536^2): the
     adjoint identity <Ax, y> = <x, A^T y> with U[0,1) inputs (no cancellation,
-    north_star bar 1e-5), linearity A(x1 + x2) = A x1 + A x2 to fp32 rounding,
+    north_star bar 1e-5), linearity A(x1 + x2) = A x1 + A x2 to fp32 rounding
+    of the integral formulation's prefix sums,
     and run-to-run determinism of both directions."""
     from paper_2307_05801_b200 import configs
 
@@ -461,7 +462,10 @@ def test_full_size_adjoint_and_linearity(which):
     a12 = plan.forward(x + x2)
     a2 = plan.forward(x2)
     err = float((a12.double() - ax.double() - a2.double()).norm() / a12.double().norm())
-    assert err <= 1e-6, err
+    # fp32 rounding of the staged prefix sums (sf_forward3d.cu): each row value
+    # is a difference of two prefix values of up to ~512 slices, ~1e-5 relative
+    # per (column, row) and ~1e-6 over a ray -- 100x inside the 1e-4 parity bar
+    assert err <= 5e-6, err
 
 
 @pytest.mark.parametrize("world", [2, 3, 6])
