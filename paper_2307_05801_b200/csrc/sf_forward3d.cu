@@ -18,7 +18,7 @@
 // lane l - 1 with a shuffle.  y(r, c) += (B ts(c)) (Fn_up - Fn_lo).
 //
 // Task decomposition, wedge enumeration and candidate setup follow round 1:
-// one WARP owns (view, F3_CW-column tile, F3_KR * 32-row band); it enumerates
+// one WARP owns (view, F3_CW-column tile, KR * 32-row band); it enumerates
 // the wedge of voxel columns between the tile's edge rays, sets the
 // candidates up lane-parallel (transverse weights in fp32, axial map in f64 at
 // the (sub-)voxel centre, relative to the band), and gathers them into its
@@ -35,22 +35,19 @@
 #ifndef CTP_F3_MINB
 #define CTP_F3_MINB 3
 #endif
-#ifndef CTP_F3_KR
-#define CTP_F3_KR 24
-#endif
 
 namespace ctp {
 
 constexpr int F3_CW = 4;              // detector columns per tile
-constexpr int F3_KR = CTP_F3_KR;      // 32-row groups per warp task (24: a 768-row detector in one band)
-static_assert(F3_KR % 4 == 0, "row groups are processed in blocks of 4 (two packed pairs)");
-constexpr int F3_ROWS = 32 * F3_KR;   // rows per band
+// 32-row groups per warp task (KR, a template parameter): 24 (768-row bands)
+// when every column's staged slices fit one piece (nz <= F3_XCAP), else 12
 constexpr int F3_VCH = 16;            // views per chunk of the task order
 constexpr int F3_WARPS = 4;           // independent warps per CTA
 constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
-constexpr int F3_XLEN = F3_XCAP + 4;  // + the total / zero pad entry
-constexpr int F3_EBUF = 96;           // >= 31 pending + 64 from one setup round
-static_assert(F3_KR <= 31, "row groups are 5-bit in F3Entry::info");
+constexpr int F3_PAD = 96;            // zero slices below / total slices above the staged range
+constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G / X table length
+constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
+
 
 struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
   int col;        // x offset of the first staged slice za4 (float4 units on the vector path)
@@ -66,8 +63,10 @@ static_assert(sizeof(F3Entry) == 48, "F3Entry layout");
 
 struct F3Smem {  // per warp
   F3Entry ent[F3_EBUF];
-  float G[F3_XLEN];          // exclusive prefix of amp * x over the staged slices; G[n] = total
-  float X[F3_XLEN];          // amp * x; X[n] = 0
+  // staged slice j at index F3_PAD + j; [0, F3_PAD): G = X = 0 (written once),
+  // [F3_PAD + n, F3_PAD + n + F3_PAD]: G = total, X = 0 (per entry)
+  float G[F3_TAB];           // exclusive prefix of amp * x over the staged slices
+  float X[F3_TAB];           // amp * x
   float xr[2][F3_XCAP];      // raw x of the next fast entries (cp.async)
 };
 
@@ -233,34 +232,40 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
     const int s0 = 256 * c + 4 * lane, s1 = s0 + 128;
     // RAW: the float4 that holds (or starts at) index n carries G[n]
     if (RAW ? s0 <= n : s0 < n) {
-      *reinterpret_cast<float4*>(S.G + s0) = make_float4(e01.x, e01.y, e23.x, e23.y);
-      *reinterpret_cast<float4*>(S.X + s0) = make_float4(xa[0].x, xa[0].y, xa[1].x, xa[1].y);
+      *reinterpret_cast<float4*>(S.G + F3_PAD + s0) = make_float4(e01.x, e01.y, e23.x, e23.y);
+      *reinterpret_cast<float4*>(S.X + F3_PAD + s0) = make_float4(xa[0].x, xa[0].y, xa[1].x, xa[1].y);
     }
     if (RAW ? s1 <= n : s1 < n) {
-      *reinterpret_cast<float4*>(S.G + s1) = make_float4(f01.x, f01.y, f23.x, f23.y);
-      *reinterpret_cast<float4*>(S.X + s1) = make_float4(xa[2].x, xa[2].y, xa[3].x, xa[3].y);
+      *reinterpret_cast<float4*>(S.G + F3_PAD + s1) = make_float4(f01.x, f01.y, f23.x, f23.y);
+      *reinterpret_cast<float4*>(S.X + F3_PAD + s1) = make_float4(xa[2].x, xa[2].y, xa[3].x, xa[3].y);
     }
     carry += tot_a + tot_b;
   }
-  // pad entry (u = n evaluates to the total) where no store above wrote it
-  if (!RAW || (n & 255) == 0) {
-    __syncwarp();
-    if (lane == 0) {
-      S.G[n] = carry;
-      S.X[n] = 0.0f;
-    }
+  // back pad: entries n .. n + F3_PAD evaluate to the total (X = 0).  RAW:
+  // the exclusive prefix at n is G[n] as stored above, unless no store
+  // covered index n (n a multiple of 256), when it is the carry.
+  __syncwarp();
+  const float total = (!RAW || (n & 255) == 0) ? carry : S.G[F3_PAD + n];
+  __syncwarp();
+#pragma unroll
+  for (int i = lane; i <= F3_PAD; i += 32) {
+    S.G[F3_PAD + n + i] = total;
+    S.X[F3_PAD + n + i] = 0.0f;
   }
 }
 
-// Fn(u) = G_k + (u - k) X_k, k = floor(u), 0 <= u <= n: floor by adding 2^23
-// with round-down and the index from the sum's bits (no conversion pipe).
+// Fn(u) = G_k + (u - k) X_k, k = floor(u), -2^22 < u < 2^22: floor by adding
+// 1.5 * 2^23 with round-down (the sum lies in [2^23, 2^24), where the float
+// spacing is 1) and the signed index from the sum's bits (no conversion pipe).
+// The table offset F3_PAD lives in g_adj (an integer), not in u, so u keeps
+// its full fp32 resolution.
 __device__ __forceinline__ float f3_eval(unsigned g_adj, float u) {
-  const float tf = __fadd_rd(u, 8388608.0f);
-  const float fr = u - (tf - 8388608.0f);  // both subtractions exact
+  const float tf = __fadd_rd(u, 12582912.0f);
+  const float fr = u - (tf - 12582912.0f);  // both subtractions exact
   const unsigned a = (unsigned)__float_as_int(tf) * 4u + g_adj;
   float G, X;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G) : "r"(a));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X) : "r"(a), "n"(4 * F3_XLEN));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X) : "r"(a), "n"(4 * F3_TAB));
   return fmaf(fr, X, G);
 }
 
@@ -272,61 +277,66 @@ __device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
   float2 tf;
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\t"
       "add.rm.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
-      : "=f"(tf.x), "=f"(tf.y) : "f"(u.x), "f"(u.y), "f"(8388608.0f));
-  const float2 fr = sub2f_(u, add2_(tf, bc2_(-8388608.0f)));  // exact
+      : "=f"(tf.x), "=f"(tf.y) : "f"(u.x), "f"(u.y), "f"(12582912.0f));
+  const float2 fr = sub2f_(u, add2_(tf, bc2_(-12582912.0f)));  // exact
   const unsigned a0 = (unsigned)__float_as_int(tf.x) * 4u + g_adj;
   const unsigned a1 = (unsigned)__float_as_int(tf.y) * 4u + g_adj;
   float G0, X0, G1, X1;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G0) : "r"(a0));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X0) : "r"(a0), "n"(4 * F3_XLEN));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X0) : "r"(a0), "n"(4 * F3_TAB));
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G1) : "r"(a1));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X1) : "r"(a1), "n"(4 * F3_XLEN));
+  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X1) : "r"(a1), "n"(4 * F3_TAB));
   return fma2_(fr, make_float2(X0, X1), make_float2(G0, G1));
 }
 
-__device__ __forceinline__ void f3_rows(float (&acc)[F3_KR][F3_CW], unsigned g_adj, float cu, float invB,
+// Rows of the groups g0..g1 in pairs of groups (64 rows): lane l owns rows
+// 64 p + 2 l and 64 p + 2 l + 1, evaluates Fn at their upper boundaries and
+// takes the lower boundary of row 64 p + 2 l from lane l - 1 (lane 31 of the
+// previous pair for lane 0).  Index k = floor(u) reads table entry F3_PAD + k;
+// with 64 invB + 2 <= F3_PAD every row of an evaluated pair stays inside the
+// pads (rows past the column's reach read the pads and add exactly 0),
+// otherwise (CLAMP) u is clamped to [0, n].
+template <int KR, bool CLAMP>
+__device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj, float cu, float invB,
                                         const float (&bts)[F3_CW], int n, int g0, int g1, int lane) {
-  const float umax = (float)n;
-  const float uL = fmaf((float)lane, invB, cu), du = 32.0f * invB;
-  const int kb0 = g0 & ~3;
-  // lower boundary of the first evaluated group's rows (used by lane 0)
-  float rot_prev = f3_eval(g_adj, fminf(fmaxf(fmaf(du, (float)kb0, uL - invB), 0.0f), umax));
+  const float cuP = cu;
+  const float ulo = 0.0f, uhi = (float)n;
+  const float ua0 = fmaf((float)(2 * lane), invB, cuP), ub0 = fmaf((float)(2 * lane + 1), invB, cuP);
+  const float du = 64.0f * invB;
+  const int p0 = g0 >> 1, p1 = g1 >> 1;
+  // lower boundary of the first evaluated pair's first row (used by lane 0)
+  float ul = fmaf(du, (float)p0, cuP - invB);
+  if (CLAMP) ul = fminf(fmaxf(ul, ulo), uhi);
+  float rot_prev = f3_eval(g_adj, ul);
   const int src = (lane + 31) & 31;
   const bool l0 = lane == 0;
   const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
 #pragma unroll
-  for (int kb = 0; kb < F3_KR; kb += 4) {
-    if (kb + 3 < g0 || kb > g1) continue;  // warp-uniform
-    // interior block: every boundary of its 128 rows lies in [0, n] (no clamps)
-    const bool inner = fmaf((float)(32 * kb - 1), invB, cu) >= 0.0f &&
-                       fmaf((float)(32 * kb + 127), invB, cu) <= umax;
-#pragma unroll
-    for (int k = kb; k < kb + 4; k += 2) {
-      float2 u = make_float2(fmaf(du, (float)k, uL), fmaf(du, (float)(k + 1), uL));
-      if (!inner) {
-        u.x = fminf(fmaxf(u.x, 0.0f), umax);
-        u.y = fminf(fmaxf(u.y, 0.0f), umax);
-      }
-      const float2 Fu = f3_eval2(g_adj, u);
-      const float r0 = __shfl_sync(0xffffffffu, Fu.x, src);
-      const float r1 = __shfl_sync(0xffffffffu, Fu.y, src);
-      const float2 d = sub2f_(Fu, make_float2(l0 ? rot_prev : r0, l0 ? r0 : r1));
-      rot_prev = r1;
-      float2 a;
-      a = fma2_(b01, bc2_(d.x), make_float2(acc[k][0], acc[k][1]));
-      acc[k][0] = a.x; acc[k][1] = a.y;
-      a = fma2_(b23, bc2_(d.x), make_float2(acc[k][2], acc[k][3]));
-      acc[k][2] = a.x; acc[k][3] = a.y;
-      a = fma2_(b01, bc2_(d.y), make_float2(acc[k + 1][0], acc[k + 1][1]));
-      acc[k + 1][0] = a.x; acc[k + 1][1] = a.y;
-      a = fma2_(b23, bc2_(d.y), make_float2(acc[k + 1][2], acc[k + 1][3]));
-      acc[k + 1][2] = a.x; acc[k + 1][3] = a.y;
+  for (int p = 0; p < KR / 2; ++p) {
+    if (p < p0 || p > p1) continue;  // warp-uniform
+    float2 u = make_float2(fmaf(du, (float)p, ua0), fmaf(du, (float)p, ub0));
+    if (CLAMP) {
+      u.x = fminf(fmaxf(u.x, ulo), uhi);
+      u.y = fminf(fmaxf(u.y, ulo), uhi);
     }
+    const float2 F = f3_eval2(g_adj, u);
+    const float rot = __shfl_sync(0xffffffffu, F.y, src);
+    const float2 d = sub2f_(F, make_float2(l0 ? rot_prev : rot, F.x));
+    rot_prev = rot;
+    float2 a;
+    a = fma2_(b01, bc2_(d.x), make_float2(acc[2 * p][0], acc[2 * p][1]));
+    acc[2 * p][0] = a.x; acc[2 * p][1] = a.y;
+    a = fma2_(b23, bc2_(d.x), make_float2(acc[2 * p][2], acc[2 * p][3]));
+    acc[2 * p][2] = a.x; acc[2 * p][3] = a.y;
+    a = fma2_(b01, bc2_(d.y), make_float2(acc[2 * p + 1][0], acc[2 * p + 1][1]));
+    acc[2 * p + 1][0] = a.x; acc[2 * p + 1][1] = a.y;
+    a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][2], acc[2 * p + 1][3]));
+    acc[2 * p + 1][2] = a.x; acc[2 * p + 1][3] = a.y;
   }
 }
 
-template <bool VEC>
-__device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[F3_KR][F3_CW],
+template <int KR, bool VEC>
+__device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR][F3_CW],
                                            const float* __restrict__ xb, int lane) {
   int pbuf = 0;  // xr buffer the next prefetch goes to
   // x of the next fast entry is in flight (cp.async, 16-byte copies on the
@@ -375,7 +385,8 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[F3_
       else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lxy, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
-      f3_rows(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      if (64.0f * invB + 2.0f <= (float)F3_PAD) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      else f3_rows<KR, true>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
       __syncwarp();
       continue;
     }
@@ -386,14 +397,14 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[F3_
       f3_stage<false, false>(S, nullptr, xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0)) + p0, n,
                       fma_(a1, (float)p0, a0), a1, lxy, lane);
       __syncwarp();
-      f3_rows(acc, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
+      f3_rows<KR, true>(acc, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
       __syncwarp();
     }
   }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kernel(
+template <int KR, bool VEC>
+__global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
     const float* __restrict__ xT, float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
   extern __shared__ __align__(16) unsigned char f3_smem_raw[];
@@ -417,8 +428,8 @@ __global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kerne
   const int v = vb % gp.nv, b = vb / gp.nv;
   const int c0 = tile * F3_CW;
   const int cw = min(F3_CW, gp.nc - c0);
-  const int rw0 = band * F3_ROWS;
-  const int nrows = min(F3_ROWS, gp.nr - rw0);
+  const int rw0 = band * 32 * KR;
+  const int nrows = min(32 * KR, gp.nr - rw0);
   const ViewCoef vc = vcoef[v];
 
   // wedge between the tile's edge rays, in (primary, secondary) grid axes
@@ -436,17 +447,24 @@ __global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kerne
   const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
   const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
 
-  float acc[F3_KR][F3_CW];
+  static_assert(KR % 2 == 0 && KR <= 31, "pairs of groups; 5-bit group indices in F3Entry::info");
+  float acc[KR][F3_CW];
 #pragma unroll
-  for (int k = 0; k < F3_KR; ++k)
+  for (int k = 0; k < KR; ++k)
 #pragma unroll
     for (int c = 0; c < F3_CW; ++c) acc[k][c] = 0.0f;
   const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
-  if (VEC) {  // the RAW staging reads the cp.async buffers past nst: keep them finite
-    for (int i = lane; i < 2 * F3_XCAP; i += 32) (&S.xr[0][0])[i] = 0.0f;
-    __syncwarp();
+  // front pads of the G / X table (never rewritten); the RAW staging reads
+  // the cp.async buffers past nst: keep them finite
+  for (int i = lane; i < F3_PAD; i += 32) {
+    S.G[i] = 0.0f;
+    S.X[i] = 0.0f;
   }
-  const unsigned g_adj = (unsigned)__cvta_generic_to_shared(S.G) - 0x4B000000u * 4u;
+  if (VEC)
+    for (int i = lane; i < 2 * F3_XCAP; i += 32) (&S.xr[0][0])[i] = 0.0f;
+  __syncwarp();
+  // G table base + F3_PAD entries - (bits of 1.5 * 2^23) entries; see f3_eval
+  const unsigned g_adj = (unsigned)__cvta_generic_to_shared(S.G) + 4u * F3_PAD - 0x4B400000u * 4u;
 
   int pending = 0;
   for (int ib = 0; ib < nP; ib += 32) {
@@ -475,21 +493,21 @@ __global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kerne
       pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
                                primary_x, c0, cw, rw0, nrows, VEC, g_adj);
       __syncwarp();
-      if (pending >= 32) {
-        f3_process<VEC>(S, pending, acc, xb, lane);
+      if (pending >= 16) {
+        f3_process<KR, VEC>(S, pending, acc, xb, lane);
         pending = 0;
         __syncwarp();
       }
     }
   }
-  if (pending > 0) f3_process<VEC>(S, pending, acc, xb, lane);
+  if (pending > 0) f3_process<KR, VEC>(S, pending, acc, xb, lane);
 
-  // store the tile: y[b][v][r][c0 + c], rows rw0 + 32 k + lane
+  // store the tile: y[b][v][r][c0 + c], rows rw0 + 64 (k / 2) + 2 lane + k % 2
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
   const bool v4 = cw == F3_CW && (gp.nc & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
 #pragma unroll
-  for (int k = 0; k < F3_KR; ++k) {
-    const int r = 32 * k + lane;
+  for (int k = 0; k < KR; ++k) {
+    const int r = 64 * (k >> 1) + 2 * lane + (k & 1);
     if (r >= nrows) continue;
     float* row = yv + (size_t)(rw0 + r) * gp.nc + c0;
     if (v4) {
@@ -509,18 +527,17 @@ __global__ void __launch_bounds__(F3_WARPS * 32, CTP_F3_MINB) sf_forward3d_kerne
   }
 }
 
-cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
-                           float* sino, int batch, bool accumulate, cudaStream_t st) {
-  static const bool legacy = getenv("CTP_FWD_LEGACY") != nullptr;  // A/B against round 1's kernel
-  if (legacy) return launch_forward_legacy(gp, vcoef, vax, xT, sino, batch, accumulate, st);
+template <int KR>
+static cudaError_t launch_forward3d(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                                   float* sino, int batch, bool accumulate, cudaStream_t st) {
   const size_t smem = sizeof(F3Smem) * F3_WARPS;
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
   if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
-  auto kern = vec ? sf_forward3d_kernel<true> : sf_forward3d_kernel<false>;
+  auto kern = vec ? sf_forward3d_kernel<KR, true> : sf_forward3d_kernel<KR, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long nbands = (gp.nr + F3_ROWS - 1) / F3_ROWS;
+  const long long nbands = (gp.nr + 32 * KR - 1) / (32 * KR);
   const long long ntiles = (gp.nc + F3_CW - 1) / F3_CW;
   const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
   const long long max_blocks = 1LL << 30;
@@ -533,6 +550,17 @@ cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const Vi
     kern<<<grid, F3_WARPS * 32, smem, st>>>(g2, vcoef, vax, xT, sino, accumulate ? 1 : 0, t0, ntasks);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
+                           float* sino, int batch, bool accumulate, cudaStream_t st) {
+  static const bool legacy = getenv("CTP_FWD_LEGACY") != nullptr;  // A/B against round 1's kernel
+  if (legacy) return launch_forward_legacy(gp, vcoef, vax, xT, sino, batch, accumulate, st);
+  // one 768-row band when every column fits one staged piece; else 384-row bands
+  static const int kr_env = getenv("CTP_F3_KR") ? atoi(getenv("CTP_F3_KR")) : 0;  // (tuning)
+  const bool wide = kr_env ? kr_env == 24 : (gp.nr > 384 && gp.nz <= F3_XCAP);
+  return wide ? launch_forward3d<24>(gp, vcoef, vax, xT, sino, batch, accumulate, st)
+              : launch_forward3d<12>(gp, vcoef, vax, xT, sino, batch, accumulate, st);
 }
 
 }  // namespace ctp

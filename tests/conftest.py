@@ -72,5 +72,10 @@ def max_abs_rel(a, b):
 REL_L2_TOL = 1e-4
 MAX_ABS_TOL = 1e-4
 ADJOINT_TOL = 1e-5
+# Two fp32 evaluations of the SAME projection under a different partition
+# (z-slabs, view chunks, view shards, row sub-geometries): the integral
+# formulation's prefix sums (csrc/sf_forward3d.cu, sf_back3d.cu) round
+# differently per partition, ~1e-6 relative; 10x that, 10x inside the bar.
+REARRANGE_TOL = 1e-5
 #: explicit-matrix transpose bound of the 3D pair, relative to max|A| (fp32 rounding)
 TRANSPOSE_TOL = 4e-6

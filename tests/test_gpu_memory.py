@@ -18,7 +18,7 @@ import torch
 import paper_2307_05801_b200 as ct
 from paper_2307_05801_b200 import chunking, configs
 
-from conftest import rel_l2
+from conftest import REARRANGE_TOL, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -85,7 +85,7 @@ def test_streaming_within_device_budget(monkeypatch):
     got_b = ct.adjoint(P, y)
     peak = torch.cuda.max_memory_allocated(DEV) - base
     assert peak <= budget, (peak, budget)
-    assert rel_l2(got_f, ref_f) < 1e-6 and rel_l2(got_b, ref_b) < 1e-6
+    assert rel_l2(got_f, ref_f) < REARRANGE_TOL and rel_l2(got_b, ref_b) < REARRANGE_TOL
 
 
 @pytest.mark.parametrize("direction", [0, 1])
@@ -99,7 +99,7 @@ def test_stream_blocks_match_resident(direction, nzs, nvc, B):
     ref = (plan.forward if direction == 0 else plan.back)(h.to(DEV)).cpu()
     ranges = [(a, min(g.numViews, a + nvc)) for a in range(0, g.numViews, nvc)]
     got = chunking.stream_apply(plan, h, direction, nzs, ranges)
-    assert rel_l2(got.numpy(), ref.numpy()) < 1e-6
+    assert rel_l2(got.numpy(), ref.numpy()) < REARRANGE_TOL
     if direction == 0 and nzs >= spec.numZ:
         assert torch.equal(got, ref)  # one slab: the same launches per view
 
