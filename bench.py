@@ -260,7 +260,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="batch size (default: 64 for c2, else 1)")
@@ -378,9 +378,13 @@ def main():
     peak, peak_kind = _peaks()
     f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(back_ms)
     upd = B * nvox * nv_local
+    # the kernels that ran (csrc/sf_forward3d.cu; csrc/sf_kernels.cu's per-row back
+    # kernel unless CTP_BACK_INTEGRAL selects csrc/sf_back3d.cu)
+    fname = "sf_forward_kernel" if os.environ.get("CTP_FWD_LEGACY") else "sf_forward3d_kernel"
+    bname = "sf_back3d_kernel" if os.environ.get("CTP_BACK_INTEGRAL") else "sf_back_kernel"
     kern = {
-        "sf_forward_kernel": {"ms": f_ms, "bytes": 4.0 * upd + 4.0 * B * nv_local * nr * nc},
-        "sf_back_kernel": {"ms": b_ms, "bytes": 4.0 * upd + 4.0 * B * nvox},
+        fname: {"ms": f_ms, "bytes": 4.0 * upd + 4.0 * B * nv_local * nr * nc},
+        bname: {"ms": b_ms, "bytes": 4.0 * upd + 4.0 * B * nvox},
     }
     for k in kern.values():
         k["gbs"] = k["bytes"] / (k["ms"] / 1e3) / 1e9
@@ -388,15 +392,23 @@ def main():
         k["gups"] = upd / (k["ms"] / 1e3) / 1e9
     dom = max(kern, key=lambda n: kern[n]["ms"])
     traffic = None
+    prof = {}
     try:
-        # DRAM bytes per launch from the committed `ncu --set full` capture of the
-        # same workload (tools/summarize_profiles.py); only when it covers all views
+        # DRAM bytes per launch, warp instructions per update and issue activity
+        # from the committed `ncu --set full` capture of the same kernel on C3
+        # (tools/summarize_profiles.py; a view subset is scaled to all views)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f).get(dom)
-        if t and t.get("views_in_capture") == g.numViews and args.config == "c3" and B == 1:
+            prof = json.load(f)
+        t = prof.get(dom)
+        if t and args.config == "c3" and B == 1 and world == 1:
             traffic = t["dram_bytes_per_launch"]
     except Exception:
         pass
+    for k, v in kern.items():
+        t = prof.get(k) if args.config == "c3" and B == 1 else None
+        if t and "inst_per_update" in t:
+            v["inst_per_update"] = t["inst_per_update"]
+            v["issue_active"] = t["issue_active"]
 
     # e2e: public API with host (pinned) buffers, H2D + D2H inside the timed region
     e2e = None
@@ -455,7 +467,12 @@ def main():
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": kern[dom]["frac"],
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": kern[dom]["bytes"],
-                         "launch_ms": kern[dom]["ms"]},
+                         "launch_ms": kern[dom]["ms"],
+                         # the kernels are issue-bound, not HBM-bound:
+                         # ncu warp instructions per voxel-view update and issue-slot activity
+                         "inst_per_update": kern[dom].get("inst_per_update"),
+                         "issue_active": kern[dom].get("issue_active"),
+                         "profile": prof.get(dom, {}).get("capture")},
             "kernels": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in kern.items()},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -44,7 +44,7 @@ constexpr int F3_CW = 4;              // detector columns per tile
 constexpr int F3_VCH = 16;            // views per chunk of the task order
 constexpr int F3_WARPS = 4;           // independent warps per CTA
 constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
-constexpr int F3_PAD = 96;            // zero slices below / total slices above the staged range
+constexpr int F3_PAD = 160;           // zero slices below / total slices above the staged range
 constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G / X table length
 constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
 
@@ -67,7 +67,7 @@ struct F3Smem {  // per warp
   // [F3_PAD + n, F3_PAD + n + F3_PAD]: G = total, X = 0 (per entry)
   float G[F3_TAB];           // exclusive prefix of amp * x over the staged slices
   float X[F3_TAB];           // amp * x
-  float xr[2][F3_XCAP];      // raw x of the next fast entries (cp.async)
+  float xr[F3_XCAP];         // raw x of the next fast entry (cp.async; read by the staging, then refilled)
 };
 
 __device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
@@ -289,11 +289,13 @@ __device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
   return fma2_(fr, make_float2(X0, X1), make_float2(G0, G1));
 }
 
-// Rows of the groups g0..g1 in pairs of groups (64 rows): lane l owns rows
+// Rows of the groups g0..g1 in blocks of two pairs of groups (128 rows,
+// straight-line code so the pairs' dependency chains interleave; blocks
+// outside [g0, g1] are skipped).  In a pair (64 rows) lane l owns rows
 // 64 p + 2 l and 64 p + 2 l + 1, evaluates Fn at their upper boundaries and
 // takes the lower boundary of row 64 p + 2 l from lane l - 1 (lane 31 of the
 // previous pair for lane 0).  Index k = floor(u) reads table entry F3_PAD + k;
-// with 64 invB + 2 <= F3_PAD every row of an evaluated pair stays inside the
+// with 128 invB + 2 <= F3_PAD every row of an evaluated block stays inside the
 // pads (rows past the column's reach read the pads and add exactly 0),
 // otherwise (CLAMP) u is clamped to [0, n].
 template <int KR, bool CLAMP>
@@ -303,7 +305,7 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
   const float ulo = 0.0f, uhi = (float)n;
   const float ua0 = fmaf((float)(2 * lane), invB, cuP), ub0 = fmaf((float)(2 * lane + 1), invB, cuP);
   const float du = 64.0f * invB;
-  const int p0 = g0 >> 1, p1 = g1 >> 1;
+  const int p0 = (g0 >> 1) & ~1, p1 = g1 >> 1;  // (p0: first pair of its 128-row block)
   // lower boundary of the first evaluated pair's first row (used by lane 0)
   float ul = fmaf(du, (float)p0, cuP - invB);
   if (CLAMP) ul = fminf(fmaxf(ul, ulo), uhi);
@@ -312,33 +314,35 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
   const bool l0 = lane == 0;
   const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
 #pragma unroll
-  for (int p = 0; p < KR / 2; ++p) {
-    if (p < p0 || p > p1) continue;  // warp-uniform
-    float2 u = make_float2(fmaf(du, (float)p, ua0), fmaf(du, (float)p, ub0));
-    if (CLAMP) {
-      u.x = fminf(fmaxf(u.x, ulo), uhi);
-      u.y = fminf(fmaxf(u.y, ulo), uhi);
+  for (int q = 0; q < KR / 4; ++q) {  // blocks of two pairs (128 rows), straight-line inside
+    if (2 * q + 1 < p0 || 2 * q > p1) continue;  // warp-uniform
+#pragma unroll
+    for (int p = 2 * q; p < 2 * q + 2; ++p) {
+      float2 u = make_float2(fmaf(du, (float)p, ua0), fmaf(du, (float)p, ub0));
+      if (CLAMP) {
+        u.x = fminf(fmaxf(u.x, ulo), uhi);
+        u.y = fminf(fmaxf(u.y, ulo), uhi);
+      }
+      const float2 F = f3_eval2(g_adj, u);
+      const float rot = __shfl_sync(0xffffffffu, F.y, src);
+      const float2 d = sub2f_(F, make_float2(l0 ? rot_prev : rot, F.x));
+      rot_prev = rot;
+      float2 a;
+      a = fma2_(b01, bc2_(d.x), make_float2(acc[2 * p][0], acc[2 * p][1]));
+      acc[2 * p][0] = a.x; acc[2 * p][1] = a.y;
+      a = fma2_(b23, bc2_(d.x), make_float2(acc[2 * p][2], acc[2 * p][3]));
+      acc[2 * p][2] = a.x; acc[2 * p][3] = a.y;
+      a = fma2_(b01, bc2_(d.y), make_float2(acc[2 * p + 1][0], acc[2 * p + 1][1]));
+      acc[2 * p + 1][0] = a.x; acc[2 * p + 1][1] = a.y;
+      a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][2], acc[2 * p + 1][3]));
+      acc[2 * p + 1][2] = a.x; acc[2 * p + 1][3] = a.y;
     }
-    const float2 F = f3_eval2(g_adj, u);
-    const float rot = __shfl_sync(0xffffffffu, F.y, src);
-    const float2 d = sub2f_(F, make_float2(l0 ? rot_prev : rot, F.x));
-    rot_prev = rot;
-    float2 a;
-    a = fma2_(b01, bc2_(d.x), make_float2(acc[2 * p][0], acc[2 * p][1]));
-    acc[2 * p][0] = a.x; acc[2 * p][1] = a.y;
-    a = fma2_(b23, bc2_(d.x), make_float2(acc[2 * p][2], acc[2 * p][3]));
-    acc[2 * p][2] = a.x; acc[2 * p][3] = a.y;
-    a = fma2_(b01, bc2_(d.y), make_float2(acc[2 * p + 1][0], acc[2 * p + 1][1]));
-    acc[2 * p + 1][0] = a.x; acc[2 * p + 1][1] = a.y;
-    a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][2], acc[2 * p + 1][3]));
-    acc[2 * p + 1][2] = a.x; acc[2 * p + 1][3] = a.y;
   }
 }
 
 template <int KR, bool VEC>
 __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR][F3_CW],
                                            const float* __restrict__ xb, int lane) {
-  int pbuf = 0;  // xr buffer the next prefetch goes to
   // x of the next fast entry is in flight (cp.async, 16-byte copies on the
   // vector path) while the current one is processed
   auto next_fast = [&](int e) {
@@ -351,10 +355,9 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
 #pragma unroll
           for (int t = 0; t < F3_XCAP / 128; ++t) {
             const int s = 4 * lane + 128 * t;
-            if (s < nst) cp_async16(&S.xr[pbuf][s], xc + s);
+            if (s < nst) cp_async16(&S.xr[s], xc + s);
           }
           cp_async_commit();
-          pbuf ^= 1;
         }
         return e;
       }
@@ -379,13 +382,13 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
       if (VEC) {
         cp_async_wait_all();  // this lane's copies; the warp barrier publishes the others'
         __syncwarp();
-        xraw = S.xr[pbuf ^ 1];
+        xraw = S.xr;
       }
       if (VEC) f3_stage<true, true>(S, xraw, xg, nst, a0, a1, lxy, lane);
       else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lxy, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
-      if (64.0f * invB + 2.0f <= (float)F3_PAD) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      if (128.0f * invB + 2.0f <= (float)F3_PAD) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
       else f3_rows<KR, true>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
       __syncwarp();
       continue;
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
   const bool cull = vc.cull && fabsf(ldp) * nl > 1e-3f && fabsf(hdp) * nh > 1e-3f;
   const float lslope = cull ? ldq / ldp : 0.0f, hslope = cull ? hdq / hdp : 0.0f;
 
-  static_assert(KR % 2 == 0 && KR <= 31, "pairs of groups; 5-bit group indices in F3Entry::info");
+  static_assert(KR % 4 == 0 && KR <= 31, "blocks of two pairs of groups; 5-bit group indices in F3Entry::info");
   float acc[KR][F3_CW];
 #pragma unroll
   for (int k = 0; k < KR; ++k)
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
     S.X[i] = 0.0f;
   }
   if (VEC)
-    for (int i = lane; i < 2 * F3_XCAP; i += 32) (&S.xr[0][0])[i] = 0.0f;
+    for (int i = lane; i < F3_XCAP; i += 32) S.xr[i] = 0.0f;
   __syncwarp();
   // G table base + F3_PAD entries - (bits of 1.5 * 2^23) entries; see f3_eval
   const unsigned g_adj = (unsigned)__cvta_generic_to_shared(S.G) + 4u * F3_PAD - 0x4B400000u * 4u;
