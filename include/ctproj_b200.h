@@ -131,6 +131,14 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch,
 /* Duration (ms) of the projector kernel of the last CTP_FLAG_TIME_KERNEL call
  * in `direction` (0 forward, 1 back) on this plan.  Synchronises on the
  * recorded end event.  Returns CTP_ERR_INVALID_ARGUMENT if none was recorded. */
+/* FBP back projection: the Ram-Lak ramp filter of
+ * every detector row (pkg/src/ctproj/recon.py:39-61, linear convolution, the
+ * reference's zero-padded FFT) times `scale`, fused with the layout change of
+ * the back projection's input, then the SF back projection into vol.  With
+ * scale = pi d^2 / (nv hx^2) this is fbp_parallel (recon.py:64-83).
+ * Workspace: ctp_sf_workspace_bytes(plan, 1, batch). */
+int ctp_sf_fbp_back(const ctp_plan* plan, const float* sino, float* vol, int batch, double scale,
+                    void* workspace, size_t workspace_bytes, uint32_t flags, void* stream);
 int ctp_plan_kernel_time_ms(const ctp_plan* plan, int direction, float* ms);
 
 /* Siddon pair (exact ray-voxel line lengths, float64 like the reference):

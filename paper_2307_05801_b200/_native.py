@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "ctp_sf_workspace_bytes",
     "ctp_sf_forward",
     "ctp_sf_back",
+    "ctp_sf_fbp_back",
     "ctp_plan_kernel_time_ms",
     "ctp_sf_forward_oneshot",
     "ctp_sf_back_oneshot",
@@ -134,6 +135,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = [vp, vp, vp, i32, vp, sz, u32, vp]
             fn.restype = i32
+        lib.ctp_sf_fbp_back.argtypes = [vp, vp, vp, i32, ctypes.c_double, vp, sz, u32, vp]
+        lib.ctp_sf_fbp_back.restype = i32
         lib.ctp_plan_kernel_time_ms.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_float)]
         lib.ctp_plan_kernel_time_ms.restype = i32
         for name in ("ctp_sf_forward_oneshot", "ctp_sf_back_oneshot"):
@@ -284,6 +287,27 @@ class Plan:
         if out is None:
             out = torch.empty((y.shape[0],) + self.vol_shape, dtype=torch.float32, device=self.device)
         return self._run(1, y, out, accumulate, time_kernel)
+
+
+    def fbp_back(self, y, scale: float, out=None, time_kernel: bool = False):
+        """x = A^T (ramp(y) * scale): the FBP input stage (Ram-Lak row filter,
+        recon.py:39-61) fused with the back projection's layout change, then
+        the SF back projection (ctp_sf_fbp_back); device tensors."""
+        import torch
+
+        if out is None:
+            out = torch.empty((y.shape[0],) + self.vol_shape, dtype=torch.float32, device=self.device)
+        self._check_io(1, y, out)
+        batch = int(y.shape[0])
+        nbytes = self.workspace_bytes(1, batch)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        flags = FLAG_TIME_KERNEL if time_kernel else 0
+        st = self.lib.ctp_sf_fbp_back(self._h, y.data_ptr(), out.data_ptr(), batch, float(scale), ws.data_ptr(),
+                                      nbytes, flags, stream)
+        if st != CTP_OK:
+            _raise_status(self.lib, st, "ctp_sf_fbp_back")
+        return out
 
 
 class Dist:

@@ -525,6 +525,29 @@ int ctp_siddon_back(const ctp_plan* plan, double back, const float* sino, float*
   return CTP_OK;
 }
 
+int ctp_sf_fbp_back(const ctp_plan* plan, const float* sino, float* vol, int batch, double scale,
+                    void* workspace, size_t workspace_bytes, uint32_t flags, void* stream) {
+  const size_t need = plan ? ctp_sf_workspace_bytes(plan, 1, batch) : 0;
+  int st = check_run_args(plan, sino, vol, batch, workspace, workspace_bytes, need);
+  if (st == CTP_OK) st = check_sf(plan);
+  if (st != CTP_OK) return st;
+  if (!std::isfinite(scale)) return fail(CTP_ERR_INVALID_ARGUMENT, "scale must be finite");
+  DeviceGuard guard(plan->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "select device");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const GridParams& gp = plan->gp;
+  // ramp filter fused with the row-contiguous layout change (replaces the
+  // back projection's transpose), then the 3D back projection kernel
+  float* yT = static_cast<float*>(workspace);
+  cudaError_t e = ctp::launch_ramp_rows_T(sino, yT, gp.nr, gp.nc, batch * gp.nv, plan->geom.pixel_width, scale, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ramp_rows_T_kernel");
+  KernelTimer timer(plan, 1, s, flags);
+  e = ctp::launch_back(gp, plan->d_coef, plan->d_ax, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
+  timer.stop();
+  if (e != cudaSuccess) return cuda_fail(e, "sf_back_kernel (fbp)");
+  return CTP_OK;
+}
+
 int ctp_plan_kernel_time_ms(const ctp_plan* plan, int direction, float* ms) {
   if (!plan || !ms || direction < 0 || direction > 1)
     return fail(CTP_ERR_INVALID_ARGUMENT, "bad arguments");

@@ -28,6 +28,10 @@ cudaError_t launch_back_legacy(const GridParams& gp, const ViewCoef* vcoef, cons
 cudaError_t launch_forward_legacy(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
                                   float* sino, int batch, bool accumulate, cudaStream_t st);
 size_t forward_warp_smem_bytes();
+// FBP input stage (ramp_kernels.cu): Ram-Lak filter of every detector row of
+// in [nviews][nr][nc], times scale, written row-contiguous to out [nviews][nc][nr]
+cudaError_t launch_ramp_rows_T(const float* in, float* out, int nr, int nc, int nviews, double pixel_width,
+                               double scale, cudaStream_t st);
 // fan beam (nz == nr == 1) with the batch on the lanes: inputs batch-innermost
 // (xB [ny*nx][batch], yB [nv][nc][batch]), outputs in the natural layouts
 // (sino [batch][nv][nc], vol [batch][ny*nx])

@@ -120,3 +120,22 @@ def test_psnr():
     b = np.ones(10)
     assert ct.psnr(b, b) == float("inf")
     assert ct.psnr(a, b, peak=1.0) == pytest.approx(0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nc,nr", [(37, 5), (600, 3)])
+def test_fused_ramp_back_matches_cufft_filter(nc, nr):
+    """csrc/ramp_kernels.cu (direct linear convolution, fused with the back
+    projection's input layout change) == cuFFT float64 ramp filter followed
+    by the SF back projection, on detector rows that are not a multiple of 8
+    and rows much wider than one tile."""
+    cfg = dict(geometry="parallel", numX=16, numY=16, numZ=nr, voxelWidth=1.0, voxelHeight=1.0,
+               numRows=nr, numCols=nc, pixelHeight=1.0, pixelWidth=0.75, numAngles=9, angularRange=180.0)
+    g, spec = ct.parse_config(json.dumps(cfg))
+    P = ct.ProjectorPair(ct.SF, g, spec)
+    y = torch.from_numpy(np.random.default_rng(7).standard_normal(g.shape).astype(np.float32)).cuda()
+    scale = 0.37
+    got = P.plan().fbp_back(y[None], scale)[0]
+    filt = ct.ramp_filter_rows(y.double(), g.detector.pixelWidth).float() * scale
+    ref = P.plan().back(filt[None].contiguous())[0]
+    assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
