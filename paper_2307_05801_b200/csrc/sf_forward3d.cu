@@ -44,7 +44,15 @@ constexpr int F3_CW = 4;              // detector columns per tile
 constexpr int F3_VCH = 16;            // views per chunk of the task order
 constexpr int F3_WARPS = 4;           // independent warps per CTA
 constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
-constexpr int F3_PAD = 160;           // zero slices below / total slices above the staged range
+#ifndef CTP_F3_BLK
+#define CTP_F3_BLK 2
+#endif
+#ifndef CTP_F3_PAD
+#define CTP_F3_PAD 160  // (a multiple of 4: 16-byte table stores)
+#endif
+constexpr int F3_BLK = CTP_F3_BLK;    // pairs of row groups per straight-line block (64 rows each)
+constexpr int F3_PAD = CTP_F3_PAD;    // zero slices below / total slices above the staged range
+static_assert(F3_PAD % 4 == 0, "16-byte aligned table stores");
 constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G / X table length
 constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
 
@@ -254,6 +262,69 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
   }
 }
 
+// RAW staging of up to F3_XCAP slices with both 256-slice chunks in flight:
+// the four 128-slice groups' loads, amplitudes, local prefixes and warp
+// scans are independent (only the final offsets chain), so their latency
+// chains interleave.  Same layout and results as f3_stage<true, *>.
+__device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, int n, float a0, float a1, float lxy,
+                                             int lane) {
+  static_assert(F3_XCAP == 512, "four groups of 128 slices");
+  float2 xa[4][2];
+  float t[4], inc[4], p1[4], p2[4], p3[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int s = 128 * q + 4 * lane;
+    const float4 v = *reinterpret_cast<const float4*>(xraw + s);
+    const float sf = (float)s;
+    const float2 iA = make_float2(sf, sf + 1.0f), iB = make_float2(sf + 2.0f, sf + 3.0f);
+    const float2 qA = fma2_(bc2_(a1), iA, bc2_(a0)), qB = fma2_(bc2_(a1), iB, bc2_(a0));
+    const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
+    const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
+    const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
+    xa[q][0] = mul2_(ampA, make_float2(v.x, v.y));
+    xa[q][1] = mul2_(ampB, make_float2(v.z, v.w));
+    p1[q] = xa[q][0].x;
+    p2[q] = p1[q] + xa[q][0].y;
+    p3[q] = p2[q] + xa[q][1].x;
+    t[q] = p3[q] + xa[q][1].y;
+    inc[q] = t[q];
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    float nb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nb[q] = __shfl_up_sync(0xffffffffu, inc[q], d);
+    if (lane >= d) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) inc[q] += nb[q];
+    }
+  }
+  float tot[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tot[q] = __shfl_sync(0xffffffffu, inc[q], 31);
+  float base = 0.0f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float e = base + (inc[q] - t[q]);
+    const float2 e01 = add2_(bc2_(e), make_float2(0.0f, p1[q])), e23 = add2_(bc2_(e), make_float2(p2[q], p3[q]));
+    const int s = 128 * q + 4 * lane;
+    if (s <= n) {  // the float4 that holds (or starts at) index n carries G[n]
+      *reinterpret_cast<float4*>(S.G + F3_PAD + s) = make_float4(e01.x, e01.y, e23.x, e23.y);
+      *reinterpret_cast<float4*>(S.X + F3_PAD + s) = make_float4(xa[q][0].x, xa[q][0].y, xa[q][1].x, xa[q][1].y);
+    }
+    base += tot[q];
+  }
+  // back pad (see f3_stage): G[n] as stored, or the total when n == 512
+  __syncwarp();
+  const float total = n >= F3_XCAP ? base : S.G[F3_PAD + n];
+  __syncwarp();
+#pragma unroll
+  for (int i = lane; i <= F3_PAD; i += 32) {
+    S.G[F3_PAD + n + i] = total;
+    S.X[F3_PAD + n + i] = 0.0f;
+  }
+}
+
 // Fn(u) = G_k + (u - k) X_k, k = floor(u), -2^22 < u < 2^22: floor by adding
 // 1.5 * 2^23 with round-down (the sum lies in [2^23, 2^24), where the float
 // spacing is 1) and the signed index from the sum's bits (no conversion pipe).
@@ -289,13 +360,13 @@ __device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
   return fma2_(fr, make_float2(X0, X1), make_float2(G0, G1));
 }
 
-// Rows of the groups g0..g1 in blocks of two pairs of groups (128 rows,
+// Rows of the groups g0..g1 in blocks of F3_BLK pairs of groups (64 rows each,
 // straight-line code so the pairs' dependency chains interleave; blocks
 // outside [g0, g1] are skipped).  In a pair (64 rows) lane l owns rows
 // 64 p + 2 l and 64 p + 2 l + 1, evaluates Fn at their upper boundaries and
 // takes the lower boundary of row 64 p + 2 l from lane l - 1 (lane 31 of the
 // previous pair for lane 0).  Index k = floor(u) reads table entry F3_PAD + k;
-// with 128 invB + 2 <= F3_PAD every row of an evaluated block stays inside the
+// when every row of the evaluated blocks maps inside the
 // pads (rows past the column's reach read the pads and add exactly 0),
 // otherwise (CLAMP) u is clamped to [0, n].
 template <int KR, bool CLAMP>
@@ -305,7 +376,7 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
   const float ulo = 0.0f, uhi = (float)n;
   const float ua0 = fmaf((float)(2 * lane), invB, cuP), ub0 = fmaf((float)(2 * lane + 1), invB, cuP);
   const float du = 64.0f * invB;
-  const int p0 = (g0 >> 1) & ~1, p1 = g1 >> 1;  // (p0: first pair of its 128-row block)
+  const int p0 = (g0 >> 1) / F3_BLK * F3_BLK, p1 = g1 >> 1;  // (p0: first pair of its block)
   // lower boundary of the first evaluated pair's first row (used by lane 0)
   float ul = fmaf(du, (float)p0, cuP - invB);
   if (CLAMP) ul = fminf(fmaxf(ul, ulo), uhi);
@@ -314,10 +385,11 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
   const bool l0 = lane == 0;
   const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
 #pragma unroll
-  for (int q = 0; q < KR / 4; ++q) {  // blocks of two pairs (128 rows), straight-line inside
-    if (2 * q + 1 < p0 || 2 * q > p1) continue;  // warp-uniform
+  constexpr int NB = (KR / 2 + F3_BLK - 1) / F3_BLK;
+  for (int q = 0; q < NB; ++q) {  // blocks of F3_BLK pairs, straight-line inside
+    if (F3_BLK * q + F3_BLK - 1 < p0 || F3_BLK * q > p1) continue;  // warp-uniform
 #pragma unroll
-    for (int p = 2 * q; p < 2 * q + 2; ++p) {
+    for (int p = F3_BLK * q; p < F3_BLK * q + F3_BLK && p < KR / 2; ++p) {
       float2 u = make_float2(fmaf(du, (float)p, ua0), fmaf(du, (float)p, ub0));
       if (CLAMP) {
         u.x = fminf(fmaxf(u.x, ulo), uhi);
@@ -384,11 +456,17 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
         __syncwarp();
         xraw = S.xr;
       }
-      if (VEC) f3_stage<true, true>(S, xraw, xg, nst, a0, a1, lxy, lane);
+      if (VEC) f3_stage_raw(S, xraw, nst, a0, a1, lxy, lane);
       else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lxy, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
-      if (128.0f * invB + 2.0f <= (float)F3_PAD) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      // unclamped when every evaluated row (whole blocks around [g0, g1]) maps
+      // into the padded table
+      const int q0 = (g0 >> 1) / F3_BLK, q1 = (g1 >> 1) / F3_BLK;
+      const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), 32 * KR) - 1;
+      const bool inside = fmaf((float)rlo - 1.0f, invB, cu) >= 1.0f - (float)F3_PAD &&
+                          fmaf((float)rhi, invB, cu) <= (float)(nst + F3_PAD) - 1.0f;
+      if (inside) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
       else f3_rows<KR, true>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
       __syncwarp();
       continue;
