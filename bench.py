@@ -378,10 +378,10 @@ def main():
     peak, peak_kind = _peaks()
     f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(back_ms)
     upd = B * nvox * nv_local
-    # the kernels that ran (csrc/sf_forward3d.cu; csrc/sf_kernels.cu's per-row back
-    # kernel unless CTP_BACK_INTEGRAL selects csrc/sf_back3d.cu)
+    # the kernels that ran (csrc/sf_forward3d.cu, csrc/sf_back3d.cu; the round-1
+    # per-row kernels of csrc/sf_kernels.cu only under CTP_*_LEGACY)
     fname = "sf_forward_kernel" if os.environ.get("CTP_FWD_LEGACY") else "sf_forward3d_kernel"
-    bname = "sf_back3d_kernel" if os.environ.get("CTP_BACK_INTEGRAL") else "sf_back_kernel"
+    bname = "sf_back_kernel" if os.environ.get("CTP_BACK_LEGACY") else "sf_back3d_kernel"
     kern = {
         fname: {"ms": f_ms, "bytes": 4.0 * upd + 4.0 * B * nv_local * nr * nc},
         bname: {"ms": b_ms, "bytes": 4.0 * upd + 4.0 * B * nvox},

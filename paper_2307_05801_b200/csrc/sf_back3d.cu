@@ -36,10 +36,10 @@
 #include "sf_launch.h"
 
 #ifndef CTP_B3_WARPS
-#define CTP_B3_WARPS 8
+#define CTP_B3_WARPS 16  // a 1 x 16 strip of voxel columns along y per CTA (shared detector columns in L1)
 #endif
 #ifndef CTP_B3_MINB
-#define CTP_B3_MINB 3
+#define CTP_B3_MINB 2  // 64 registers: 32 resident warps per SM (measured best of 8/16 warps x 2-5 CTAs)
 #endif
 // rare paths (split halves, direct rows) inlined into the view loop: keeps the
 // accumulators in place (no phi copies), at the cost of code size
@@ -83,7 +83,7 @@ template <int ZPL>
 struct B3Smem {
   B3Entry ents[B3_WARPS][32];
   B3Entry split[B3_WARPS];
-  float tab[B3_WARPS][2][B3Cfg<ZPL>::QMAX];  // [0]: S_k, [1]: Q_k of the table rows
+  float tab[B3_WARPS][B3Cfg<ZPL>::QMAX + 4];  // S_k = sum_{j<k} Q_j of the table rows (S_nq = total)
 };
 
 // Footprint of one (sub-)voxel for slices izs..ize: f64 axial map at the
@@ -219,12 +219,11 @@ __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const 
       if (lane >= d) incl += n;
     }
     const float ex = carry + (incl - tot);
-    if (g < QMAX / 4) {
-      reinterpret_cast<float4*>(tab)[g] = make_float4(ex, ex + s1, ex + s2, ex + s3);
-      reinterpret_cast<float4*>(tab + QMAX)[g] = make_float4(q[0], q[1], q[2], q[3]);
-    }
+    if (g < QMAX / 4) reinterpret_cast<float4*>(tab)[g] = make_float4(ex, ex + s1, ex + s2, ex + s3);
     carry += __shfl_sync(0xffffffffu, incl, 31);
   }
+  __syncwarp();
+  if (lane == 0) tab[4 * n4] = carry;  // S at the end of the table
 }
 
 // Fast table (16-byte aligned rows, every table row on the detector): lane t
@@ -244,7 +243,6 @@ __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const flo
     T[k] = bc2_(ts[k]);
   }
   float4* sp4 = reinterpret_cast<float4*>(tab + 4 * lane);
-  float4* qp4 = reinterpret_cast<float4*>(tab + QMAX + 4 * lane);
   float carry = 0.0f;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -284,14 +282,14 @@ __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const flo
     const float2 f01 = add2_(bc2_(eb), make_float2(0.0f, b1)), f23 = add2_(bc2_(eb), make_float2(b2, b3));
     if (ok0) {  // (rows past nq are never evaluated; the arrays end at QMAX)
       sp4[64 * c] = make_float4(e01.x, e01.y, e23.x, e23.y);
-      qp4[64 * c] = make_float4(q0.x, q0.y, q1.x, q1.y);
     }
     if (ok1) {
       sp4[64 * c + 32] = make_float4(f01.x, f01.y, f23.x, f23.y);
-      qp4[64 * c + 32] = make_float4(q2.x, q2.y, q3.x, q3.y);
     }
     carry += tot_a + tot_b;
   }
+  __syncwarp();
+  if (lane == 0) tab[nq] = carry;  // S at the end of the table
 }
 
 template <int QMAX>
@@ -299,10 +297,10 @@ __device__ __forceinline__ float b3_eval(unsigned tab_adj, float w) {
   const float tf = __fadd_rd(w, 8388608.0f);
   const float fr = w - (tf - 8388608.0f);  // both subtractions exact
   const unsigned a = (unsigned)__float_as_int(tf) * 4u + tab_adj;  // one LEA
-  float S, Q;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S) : "r"(a));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q) : "r"(a), "n"(4 * QMAX));
-  return fmaf(fr, Q, S);
+  float S0, S1;  // H = S_k + fr Q_k with Q_k = S_k+1 - S_k
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S0) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(S1) : "r"(a));
+  return fmaf(fr, S1 - S0, S0);
 }
 
 __device__ __forceinline__ float2 sub2_(float2 a, float2 b) {
@@ -328,12 +326,13 @@ __device__ __forceinline__ float2 b3_eval2(unsigned tab_adj, float2 w) {
   const float2 fr = sub2_(w, add2_(tf, bc2_(-8388608.0f)));  // exact
   const unsigned a0 = (unsigned)__float_as_int(tf.x) * 4u + tab_adj;
   const unsigned a1 = (unsigned)__float_as_int(tf.y) * 4u + tab_adj;
-  float S0, Q0, S1, Q1;
+  float S0, T0, S1, T1;  // (S_k, S_k+1) of both boundaries
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S0) : "r"(a0));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q0) : "r"(a0), "n"(4 * QMAX));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(T0) : "r"(a0));
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S1) : "r"(a1));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(Q1) : "r"(a1), "n"(4 * QMAX));
-  return fma2_(fr, make_float2(Q0, Q1), make_float2(S0, S1));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(T1) : "r"(a1));
+  const float2 S = make_float2(S0, S1);
+  return fma2_(fr, sub2_(make_float2(T0, T1), S), S);
 }
 
 // Slices lane + 32 m: x += amp (H(upper) - H(lower)); the lower boundary of
@@ -437,7 +436,7 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
   const int nr = gp.nr;
   const size_t view_elems = (size_t)gp.nc * nr;
   const float* yb = yT + (size_t)b * gp.nv * view_elems;
-  float* tab = SM.tab[warp][0];
+  float* tab = SM.tab[warp];
   // table base minus 2^23 entries (b3_eval indexes it with the float bits)
   const unsigned tab_adj = (unsigned)__cvta_generic_to_shared(tab) - 0x4B000000u * 4u;
   B3Entry(&my)[32] = SM.ents[warp];
@@ -568,10 +567,8 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewA
                         float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
   if (z1 < 0) z1 = gp.nz;
   if (z0 < 0 || z0 >= z1 || z1 > gp.nz) return cudaErrorInvalidValue;
-  // the integral kernel below is not yet faster than round 1's per-row kernel
-  // on C3 (175 vs 166 ms); the latter stays the default until it is
-  static const bool integral = getenv("CTP_BACK_INTEGRAL") != nullptr;
-  if (!integral) return launch_back_legacy(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+  static const bool legacy = getenv("CTP_BACK_LEGACY") != nullptr;  // A/B against round 1's kernel
+  if (legacy) return launch_back_legacy(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
   const bool vec = gp.nr % 4 == 0 && (reinterpret_cast<uintptr_t>(yT) & 15) == 0;
   static const int zpl_env = getenv("CTP_B3_ZPL") ? atoi(getenv("CTP_B3_ZPL")) : 16;  // (tuning)
   // tall z-ranges: 512 slices per warp (16 per lane); short ones: 128
