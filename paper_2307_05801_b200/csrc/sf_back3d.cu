@@ -180,7 +180,7 @@ __device__ CTP_B3_RARE void b3_split(const GridParams& gp, const ViewCoef* __res
 // VEC, R0 and nr are multiples of 4, so a group is entirely in or out).
 template <int NC, bool VEC, int QMAX>
 __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const float* __restrict__ yc, int nr,
-                                                 int R0, int n4, const float (&ts)[B3_NCF], int lane) {
+                                                 int R0, int n4, const float* ts, int lane) {
   float carry = 0.0f;
   const int nch = (n4 + 31) >> 5;
 #pragma unroll 1
@@ -234,7 +234,7 @@ __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const 
 // addressed with immediate offsets.
 template <int NC, int NCH, int QMAX>
 __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const float* __restrict__ yc, int nr, int nq,
-                                              const float (&ts)[B3_NCF], int lane) {
+                                              const float* ts, int lane) {
   const float* p[NC];
   float2 T[NC];
 #pragma unroll
@@ -466,9 +466,7 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
         if (ncol == 0) continue;
         if (e.n4 > 0) {
           const float* yc = yview + (size_t)e.cl * nr;
-          float ts[B3_NCF];
-#pragma unroll
-          for (int k = 0; k < B3_NCF; ++k) ts[k] = e.ts[k];
+          const float* ts = e.ts;  // (read from the shared entry: no local copy)
           constexpr int NCH = (Cfg::QMAX + 255) / 256;
           if (VEC && e.R0 >= 0 && e.R0 + 4 * e.n4 <= nr) {
             const float* yr = yc + e.R0;
