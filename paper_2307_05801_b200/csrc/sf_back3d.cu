@@ -569,8 +569,9 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewA
   if (legacy) return launch_back_legacy(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
   const bool vec = gp.nr % 4 == 0 && (reinterpret_cast<uintptr_t>(yT) & 15) == 0;
   static const int zpl_env = getenv("CTP_B3_ZPL") ? atoi(getenv("CTP_B3_ZPL")) : 16;  // (tuning)
-  // tall z-ranges: 512 slices per warp (16 per lane); short ones: 128
-  if (zpl_env == 8 && z1 - z0 >= 192)
+  // slices per warp: 512 (16 per lane) for tall z-ranges, 256 for the
+  // 256-slice z-chunks of the sharded back projection (dist.cu), else 128
+  if ((zpl_env == 8 || z1 - z0 < 384) && z1 - z0 >= 192)
     return vec ? launch_back3d_z<8, true>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1)
                : launch_back3d_z<8, false>(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
   if (z1 - z0 >= 384)
