@@ -448,68 +448,67 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
   for (int m = 0; m < ZPL / 2; ++m) acc[m] = make_float2(0.0f, 0.0f);
 
   for (int vb = 0; vb < gp.nv; vb += 32) {
-    const int nsub = b3_setup<ZPL>(gp, vcoef, vax, vb, ix, iy, izs, ize, &my[lane], tab_adj) ? 2 : 1;
+    const bool split = b3_setup<ZPL>(gp, vcoef, vax, vb, ix, iy, izs, ize, &my[lane], tab_adj);
     __syncwarp();
     const int nvb = min(32, gp.nv - vb);
+    // the direct (per-row) path: wide footprints, long tables, split halves
+    auto direct = [&](const B3Entry& e, const float* yview, int v, bool second) {
+      Trap wide{};
+      if (e.ncol > B3_NCF) {  // rare: rebuild the breakpoints of this footprint
+        SubFoot f0, f1;
+        column_footprint(vcoef[v], gp, ix, iy, f0, f1);
+        wide = make_trap(second ? f1 : f0);
+      }
+      const int K = rows_per_slice(e.B);
+      const float E = 0.5f * e.B;
+#pragma unroll
+      for (int m = 0; m < ZPL; ++m) {  // (unrolled: acc stays in registers)
+        if (m >= nvalid) break;
+        const float izf = (float)(lane + 32 * m);
+        const float T = fma_(e.B, izf, e.A);
+        const float lo = sub_(T, E), hi = add_(T, E);
+        const float q = fma_(e.a1, izf, e.a0);
+        const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
+        float& am = (m & 1) ? acc[m / 2].y : acc[m / 2].x;
+        am = b3_voxel_direct(am, amp, lo, hi, e, wide, K, yview, nr, e.R0);
+      }
+    };
     const float* yview = yb + (size_t)vb * view_elems;  // [c][r] of view vb + j
     for (int j = 0; j < nvb; ++j, yview += view_elems) {
-#pragma unroll 1
-      for (int s = 0; s < nsub; ++s) {
-        if (s == 1) {
-          if (!(my[j].mask & 2)) continue;
-          __syncwarp();  // every lane is done with the previous split entry
-          if (lane == 0) b3_split<ZPL>(gp, vcoef, vax, vb + j, ix, iy, izs, ize, &sp, tab_adj);
-          __syncwarp();
-        }
-        const B3Entry& e = s == 0 ? my[j] : sp;
-        const int ncol = e.ncol;
-        if (ncol == 0) continue;
-        if (e.n4 > 0) {
-          const float* yc = yview + (size_t)e.cl * nr;
-          const float* ts = e.ts;  // (read from the shared entry: no local copy)
-          constexpr int NCH = (Cfg::QMAX + 255) / 256;
-          if (VEC && e.R0 >= 0 && e.R0 + 4 * e.n4 <= nr) {
-            const float* yr = yc + e.R0;
-            const int nq = 4 * e.n4;
-            switch (ncol) {  // warp-uniform: load only the footprint's columns
-              case 1: b3_table_fast<1, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-              case 2: b3_table_fast<2, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-              case 3: b3_table_fast<3, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-              default: b3_table_fast<4, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-            }
-          } else {
-            switch (ncol) {
-              case 1: b3_table_generic<1, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
-              case 2: b3_table_generic<2, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
-              case 3: b3_table_generic<3, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
-              default: b3_table_generic<4, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
-            }
+      const B3Entry& e = my[j];
+      const int ncol = e.ncol;
+      if (ncol > 0 && e.n4 > 0) {
+        const float* yc = yview + (size_t)e.cl * nr;
+        const float* ts = e.ts;  // (read from the shared entry: no local copy)
+        constexpr int NCH = (Cfg::QMAX + 255) / 256;
+        if (VEC && e.R0 >= 0 && e.R0 + 4 * e.n4 <= nr) {
+          const float* yr = yc + e.R0;
+          const int nq = 4 * e.n4;
+          switch (ncol) {  // warp-uniform: load only the footprint's columns
+            case 1: b3_table_fast<1, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+            case 2: b3_table_fast<2, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+            case 3: b3_table_fast<3, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+            default: b3_table_fast<4, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
           }
-          __syncwarp();
-          b3_slices<ZPL, FULL>(acc, e, lane, nvalid);
-          __syncwarp();
-          continue;
+        } else {
+          switch (ncol) {
+            case 1: b3_table_generic<1, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+            case 2: b3_table_generic<2, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+            case 3: b3_table_generic<3, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+            default: b3_table_generic<4, VEC, Cfg::QMAX>(tab, yc, nr, e.R0, e.n4, ts, lane); break;
+          }
         }
-        // direct path
-        Trap wide{};
-        if (ncol > B3_NCF) {  // rare: rebuild the breakpoints of this footprint
-          SubFoot f0, f1;
-          column_footprint(vcoef[vb + j], gp, ix, iy, f0, f1);
-          wide = make_trap(s == 0 ? f0 : f1);
-        }
-        const int K = rows_per_slice(e.B);
-        const float E = 0.5f * e.B;
-#pragma unroll
-        for (int m = 0; m < ZPL; ++m) {  // (unrolled: acc stays in registers)
-          if (m >= nvalid) break;
-          const float izf = (float)(lane + 32 * m);
-          const float T = fma_(e.B, izf, e.A);
-          const float lo = sub_(T, E), hi = add_(T, E);
-          const float q = fma_(e.a1, izf, e.a0);
-          const float amp = mul_(e.lxy, sqrt_approx(fma_(q, q, 1.0f)));
-          float& am = (m & 1) ? acc[m / 2].y : acc[m / 2].x;
-          am = b3_voxel_direct(am, amp, lo, hi, e, wide, K, yview, nr, e.R0);
-        }
+        __syncwarp();
+        b3_slices<ZPL, FULL>(acc, e, lane, nvalid);
+        __syncwarp();
+      } else if (ncol > 0) {
+        direct(e, yview, vb + j, false);
+      }
+      if (split && (e.mask & 2)) {  // second half of a split voxel (rare): rebuilt, direct path
+        __syncwarp();  // every lane is done with the previous split entry
+        if (lane == 0) b3_split<ZPL>(gp, vcoef, vax, vb + j, ix, iy, izs, ize, &sp, tab_adj);
+        __syncwarp();
+        if (sp.ncol > 0) direct(sp, yview, vb + j, true);
       }
     }
     __syncwarp();
