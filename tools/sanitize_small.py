@@ -18,5 +18,21 @@ for path, model in ((GOLDEN, ct.SF), (SIDDON_GOLDEN, ct.SIDDON)):
         y = torch.rand((2,) + g.shape, device=dev)
         ct.forward(P, x); ct.adjoint(P, y)
         n += 1
+# the integral kernels' paths (bands, pieces, clamped rows, ragged sizes,
+# long tables, partial z-blocks) and the fused FBP input stage
+from test_gpu_integral_paths import CASES
+for name, cfg in CASES.items():
+    g, spec = ct.parse_config(json.dumps(cfg))
+    P = ct.ProjectorPair(ct.SF, g, spec)
+    x = torch.rand((2,) + spec.shape, device=dev)
+    y = torch.rand((2,) + g.shape, device=dev)
+    ct.forward(P, x); ct.adjoint(P, y)
+    n += 1
+cfg = dict(geometry="parallel", numX=16, numY=16, numZ=3, voxelWidth=1.0, voxelHeight=1.0, numRows=3,
+           numCols=37, pixelHeight=1.0, pixelWidth=0.75, numAngles=9, angularRange=180.0)
+g, spec = ct.parse_config(json.dumps(cfg))
+P = ct.ProjectorPair(ct.SF, g, spec)
+P.plan().fbp_back(torch.rand((1,) + g.shape, device=dev), 0.5)
+n += 1
 torch.cuda.synchronize()
 print("ok", n)
