@@ -41,9 +41,12 @@ from .errors import CudaRuntimeError
 
 #: target bytes of sinogram per view chunk (host<->device granularity)
 CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
-#: at most this many view chunks per call when everything fits: each chunk is
-#: one launch, and a back-projection launch re-reads / re-writes its slab
-MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "8"))
+#: at most about this many view chunks per call when everything fits: each
+#: chunk is one launch (a launch tail, a re-transposed volume, a back
+#: projection's read-modify-write of its slab) while fewer chunks expose more
+#: of the first upload / last download; measured on C3 (tools/e2e_chunks.py):
+#: 1 chunk 504 ms per fwd+back call pair, 3: 478, 5: 470, 12: 496, 23: 554
+MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "4"))
 
 
 def _torch():
