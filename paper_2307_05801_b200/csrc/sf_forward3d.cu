@@ -17,6 +17,15 @@
 // band, evaluates Fn at the row's upper boundary and takes the lower one from
 // lane l - 1 with a shuffle.  y(r, c) += (B ts(c)) (Fn_up - Fn_lo).
 //
+// Tiles and their overhang.  A footprint of at most three detector columns
+// is processed ONCE, by the tile holding its first column: the tile's four
+// own columns accumulate in registers, the two columns past the tile (its
+// overhang) in shared memory, and the overhang is merged into the next
+// tile's outputs by launch order (even tiles, then odd tiles: no atomics,
+// no scratch; see the stores).  Wider footprints are taken by every tile
+// they touch, own columns only.  Without the overhang a footprint was staged
+// and evaluated by ~1.32 tiles on C3.
+//
 // Task decomposition, wedge enumeration and candidate setup follow round 1:
 // one WARP owns (view, F3_CW-column tile, KR * 32-row band); it enumerates
 // the wedge of voxel columns between the tile's edge rays, sets the
@@ -53,7 +62,8 @@ constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice 
 constexpr int F3_BLK = CTP_F3_BLK;    // pairs of row groups per straight-line block (64 rows each)
 constexpr int F3_PAD = CTP_F3_PAD;    // zero slices below / total slices above the staged range
 static_assert(F3_PAD % 4 == 0, "16-byte aligned table stores");
-constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G / X table length
+constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G table length
+constexpr int F3_OV = 2;                               // overhang columns (the next tile's first two)
 constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
 
 
@@ -64,19 +74,23 @@ struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
   float invB;     // 1 / rows per slice
   float lxy;      // amp(s) = lxy sqrt(1 + (a0 + a1 s)^2), s = staged slice index
   float a0, a1;
-  unsigned gadj;   // the warp's G table base - 2^23 entries (shared address; opaque, see f3_eval)
-  float bts[F3_CW];  // B * ts(c) of the tile's columns (0 outside the footprint)
+  unsigned gadj;   // the warp's G table base + F3_PAD - (bits of 1.5 * 2^23) entries (opaque; see f3_eval)
+  float bts[F3_CW + F3_OV];  // B * ts(c) of columns c0 .. c0 + 5 (own 4 + overhang 2; 0 outside)
+  int has_ov;      // the overhang weights are not all zero
+  int pad;
 };
-static_assert(sizeof(F3Entry) == 48, "F3Entry layout");
+static_assert(sizeof(F3Entry) == 64, "F3Entry layout");
 
 struct F3Smem {  // per warp
   F3Entry ent[F3_EBUF];
-  // staged slice j at index F3_PAD + j; [0, F3_PAD): G = X = 0 (written once),
-  // [F3_PAD + n, F3_PAD + n + F3_PAD]: G = total, X = 0 (per entry)
+  // staged slice j at index F3_PAD + j; [0, F3_PAD): 0 (written once),
+  // [F3_PAD + n, F3_PAD + n + F3_PAD + 1]: the total (per entry).
+  // Fn(u) = lerp(G_k, G_k+1, u - k).
   float G[F3_TAB];           // exclusive prefix of amp * x over the staged slices
-  float X[F3_TAB];           // amp * x
   float xr[F3_XCAP];         // raw x of the next fast entry (cp.async; read by the staging, then refilled)
 };
+// after the per-warp F3Smem blocks, for the overhang kernels only: per warp
+// float2 ov[32 KR] (rows x the next tile's first two columns)
 
 __device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
   float2 d;
@@ -91,8 +105,13 @@ __device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
 // (sub-)voxel centre.  Returns false if the (sub-)voxel misses the tile or
 // the band.
 __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const GridParams& gp, int col, int c0, int cw,
-                                        const ViewAx& ax, float2 cxy, int rw0, int nrows, bool vec) {
-  if (max(f.cl, c0) > min(f.ch, c0 + cw - 1)) return false;
+                                        const ViewAx& ax, float2 cxy, int rw0, int nrows, bool vec, bool ovmode) {
+  // ovmode: a footprint of at most three columns belongs to the tile of its
+  // first column (the columns past the tile are its overhang, merged into the
+  // next tile's outputs); a wider one is taken by every tile it touches, own
+  // columns only (and every footprint is, without ovmode)
+  const bool narrow = ovmode && f.ch - f.cl <= F3_OV;
+  if (narrow ? (f.cl < c0 || f.cl >= c0 + cw) : (max(f.cl, c0) > min(f.ch, c0 + cw - 1))) return false;
   double A, B;
   axial64(ax, gp.kind, (double)cxy.x, (double)cxy.y, A, B);
   A -= (double)rw0;  // row coordinate of slice 0's centre, band-relative
@@ -117,13 +136,21 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
   e.lxy = f.lxy;
   e.a1 = f.a1;
   e.a0 = fma_(f.a1, (float)za4, f.a0);
+  e.gadj = 0u;
   const Trap p = make_trap(f);
-  float ts[F3_CW];
-  col_weights<F3_CW>(p, c0, ts);
-  const int lo = max(f.cl, c0), hi = min(f.ch, c0 + cw - 1);
+  float ts[F3_CW + F3_OV];
+  col_weights<F3_CW + F3_OV>(p, c0, ts);
   const float Bf = (float)B;
+  bool ov = false;
 #pragma unroll
-  for (int c = 0; c < F3_CW; ++c) e.bts[c] = (c0 + c >= lo && c0 + c <= hi) ? Bf * ts[c] : 0.0f;
+  for (int c = 0; c < F3_CW + F3_OV; ++c) {
+    const int cc = c0 + c;
+    const bool mine = c < cw ? true : (narrow && cc < gp.nc);
+    const bool on = mine && cc >= f.cl && cc <= f.ch;
+    e.bts[c] = on ? Bf * ts[c] : 0.0f;
+    if (c >= F3_CW && on) ov = true;
+  }
+  e.has_ov = ov ? 1 : 0;
   // x offset of slice za4 (32-bit: the launcher checks nx*ny*nz < 2^34 resp. 2^32)
   const unsigned xo = (unsigned)(((unsigned long long)(unsigned)col * (unsigned)gp.nz + (unsigned)za4) >> (vec ? 2 : 0));
   e.col = (int)xo;
@@ -141,7 +168,7 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
 __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp,
                                           const ViewAx* __restrict__ vaxp, F3Entry* ent, int k, int total, int ib,
                                           int excl, int jl, bool primary_x, int c0, int cw, int rw0, int nrows,
-                                          bool vec, unsigned gadj) {
+                                          bool vec, bool ovmode, unsigned gadj) {
   const int lane = threadIdx.x & 31;
   int o = 0;
 #pragma unroll
@@ -162,8 +189,8 @@ __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* 
     SubFoot f0, f1;
     float2 cxy0, cxy1;
     const int m = column_subs(vc, gp, ix, iy, f0, f1, cxy0, cxy1) & 3;
-    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, vec)) mask |= 1;
-    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, vec)) mask |= 2;
+    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, vec, ovmode)) mask |= 1;
+    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, vec, ovmode)) mask |= 2;
   }
   const int n = __popc(mask);
   const int ni = warp_incl_scan(n, lane);
@@ -239,14 +266,10 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
     const float2 f01 = add2_(bc2_(eb), make_float2(0.0f, b_1)), f23 = add2_(bc2_(eb), make_float2(b_2, b_3));
     const int s0 = 256 * c + 4 * lane, s1 = s0 + 128;
     // RAW: the float4 that holds (or starts at) index n carries G[n]
-    if (RAW ? s0 <= n : s0 < n) {
+    if (RAW ? s0 <= n : s0 < n)
       *reinterpret_cast<float4*>(S.G + F3_PAD + s0) = make_float4(e01.x, e01.y, e23.x, e23.y);
-      *reinterpret_cast<float4*>(S.X + F3_PAD + s0) = make_float4(xa[0].x, xa[0].y, xa[1].x, xa[1].y);
-    }
-    if (RAW ? s1 <= n : s1 < n) {
+    if (RAW ? s1 <= n : s1 < n)
       *reinterpret_cast<float4*>(S.G + F3_PAD + s1) = make_float4(f01.x, f01.y, f23.x, f23.y);
-      *reinterpret_cast<float4*>(S.X + F3_PAD + s1) = make_float4(xa[2].x, xa[2].y, xa[3].x, xa[3].y);
-    }
     carry += tot_a + tot_b;
   }
   // back pad: entries n .. n + F3_PAD evaluate to the total (X = 0).  RAW:
@@ -255,11 +278,7 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
   __syncwarp();
   const float total = (!RAW || (n & 255) == 0) ? carry : S.G[F3_PAD + n];
   __syncwarp();
-#pragma unroll
-  for (int i = lane; i <= F3_PAD; i += 32) {
-    S.G[F3_PAD + n + i] = total;
-    S.X[F3_PAD + n + i] = 0.0f;
-  }
+  for (int i = lane; i <= F3_PAD + 1; i += 32) S.G[F3_PAD + n + i] = total;  // (G_n+1 too: lerp)
 }
 
 // RAW staging of up to F3_XCAP slices with both 256-slice chunks in flight:
@@ -308,21 +327,15 @@ __device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, int n
     const float e = base + (inc[q] - t[q]);
     const float2 e01 = add2_(bc2_(e), make_float2(0.0f, p1[q])), e23 = add2_(bc2_(e), make_float2(p2[q], p3[q]));
     const int s = 128 * q + 4 * lane;
-    if (s <= n) {  // the float4 that holds (or starts at) index n carries G[n]
+    if (s <= n)  // the float4 that holds (or starts at) index n carries G[n]
       *reinterpret_cast<float4*>(S.G + F3_PAD + s) = make_float4(e01.x, e01.y, e23.x, e23.y);
-      *reinterpret_cast<float4*>(S.X + F3_PAD + s) = make_float4(xa[q][0].x, xa[q][0].y, xa[q][1].x, xa[q][1].y);
-    }
     base += tot[q];
   }
   // back pad (see f3_stage): G[n] as stored, or the total when n == 512
   __syncwarp();
   const float total = n >= F3_XCAP ? base : S.G[F3_PAD + n];
   __syncwarp();
-#pragma unroll
-  for (int i = lane; i <= F3_PAD; i += 32) {
-    S.G[F3_PAD + n + i] = total;
-    S.X[F3_PAD + n + i] = 0.0f;
-  }
+  for (int i = lane; i <= F3_PAD + 1; i += 32) S.G[F3_PAD + n + i] = total;  // (G_n+1 too: lerp)
 }
 
 // Fn(u) = G_k + (u - k) X_k, k = floor(u), -2^22 < u < 2^22: floor by adding
@@ -334,10 +347,10 @@ __device__ __forceinline__ float f3_eval(unsigned g_adj, float u) {
   const float tf = __fadd_rd(u, 12582912.0f);
   const float fr = u - (tf - 12582912.0f);  // both subtractions exact
   const unsigned a = (unsigned)__float_as_int(tf) * 4u + g_adj;
-  float G, X;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G) : "r"(a));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X) : "r"(a), "n"(4 * F3_TAB));
-  return fmaf(fr, X, G);
+  float G0, G1;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G0) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(G1) : "r"(a));
+  return fmaf(fr, G1 - G0, G0);
 }
 
 // Rows 32 k + lane of the groups g0..g1, in blocks of four groups (a block
@@ -352,12 +365,13 @@ __device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
   const float2 fr = sub2f_(u, add2_(tf, bc2_(-12582912.0f)));  // exact
   const unsigned a0 = (unsigned)__float_as_int(tf.x) * 4u + g_adj;
   const unsigned a1 = (unsigned)__float_as_int(tf.y) * 4u + g_adj;
-  float G0, X0, G1, X1;
+  float G0, H0, G1, H1;  // (G_k, G_k+1) of both boundaries
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G0) : "r"(a0));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X0) : "r"(a0), "n"(4 * F3_TAB));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(H0) : "r"(a0));
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(G1) : "r"(a1));
-  asm volatile("ld.shared.f32 %0, [%1 + %2];" : "=f"(X1) : "r"(a1), "n"(4 * F3_TAB));
-  return fma2_(fr, make_float2(X0, X1), make_float2(G0, G1));
+  asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(H1) : "r"(a1));
+  const float2 G = make_float2(G0, G1);
+  return fma2_(fr, sub2f_(make_float2(H0, H1), G), G);
 }
 
 // Rows of the groups g0..g1 in blocks of F3_BLK pairs of groups (64 rows each,
@@ -369,9 +383,10 @@ __device__ __forceinline__ float2 f3_eval2(unsigned g_adj, float2 u) {
 // when every row of the evaluated blocks maps inside the
 // pads (rows past the column's reach read the pads and add exactly 0),
 // otherwise (CLAMP) u is clamped to [0, n].
-template <int KR, bool CLAMP>
-__device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj, float cu, float invB,
-                                        const float (&bts)[F3_CW], int n, int g0, int g1, int lane) {
+template <int KR, bool CLAMP, bool OV>
+__device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], float2* __restrict__ ovacc, unsigned g_adj,
+                                        float cu, float invB, const float (&bts)[F3_CW + F3_OV], int n, int g0,
+                                        int g1, int lane) {
   const float cuP = cu;
   const float ulo = 0.0f, uhi = (float)n;
   const float ua0 = fmaf((float)(2 * lane), invB, cuP), ub0 = fmaf((float)(2 * lane + 1), invB, cuP);
@@ -384,6 +399,8 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
   const int src = (lane + 31) & 31;
   const bool l0 = lane == 0;
   const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
+  const float2 b45 = make_float2(bts[4], bts[5]);
+  float4* ov4 = reinterpret_cast<float4*>(ovacc) + lane;  // rows 64 p + 2 lane, + 1 (two float2)
 #pragma unroll
   constexpr int NB = (KR / 2 + F3_BLK - 1) / F3_BLK;
   for (int q = 0; q < NB; ++q) {  // blocks of F3_BLK pairs, straight-line inside
@@ -408,12 +425,18 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], unsigned g_adj,
       acc[2 * p + 1][0] = a.x; acc[2 * p + 1][1] = a.y;
       a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][2], acc[2 * p + 1][3]));
       acc[2 * p + 1][2] = a.x; acc[2 * p + 1][3] = a.y;
+      if (OV) {  // the next tile's first two columns, accumulated in shared memory
+        float4 o = ov4[32 * p];
+        const float2 oa = fma2_(b45, bc2_(d.x), make_float2(o.x, o.y));
+        const float2 ob = fma2_(b45, bc2_(d.y), make_float2(o.z, o.w));
+        ov4[32 * p] = make_float4(oa.x, oa.y, ob.x, ob.y);
+      }
     }
   }
 }
 
 template <int KR, bool VEC>
-__device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR][F3_CW],
+__device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, float (&acc)[KR][F3_CW],
                                            const float* __restrict__ xb, int lane) {
   // x of the next fast entry is in flight (cp.async, 16-byte copies on the
   // vector path) while the current one is processed
@@ -445,9 +468,10 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
     const float cu = E.cu, invB = E.invB, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
     const unsigned g_adj = E.gadj;
     const int g0 = info & 31, g1 = (info >> 5) & 31;
-    float bts[F3_CW];
+    float bts[F3_CW + F3_OV];
 #pragma unroll
-    for (int c = 0; c < F3_CW; ++c) bts[c] = E.bts[c];
+    for (int c = 0; c < F3_CW + F3_OV; ++c) bts[c] = E.bts[c];
+    const bool ov = E.has_ov != 0;
     const float* xg = xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0));
     if (e == e_pf) {  // fast: one piece, x staged by cp.async (vector path)
       const float* xraw = nullptr;
@@ -466,8 +490,13 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
       const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), 32 * KR) - 1;
       const bool inside = fmaf((float)rlo - 1.0f, invB, cu) >= 1.0f - (float)F3_PAD &&
                           fmaf((float)rhi, invB, cu) <= (float)(nst + F3_PAD) - 1.0f;
-      if (inside) f3_rows<KR, false>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
-      else f3_rows<KR, true>(acc, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      if (inside) {
+        if (ov) f3_rows<KR, false, true>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
+        else f3_rows<KR, false, false>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      } else {
+        if (ov) f3_rows<KR, true, true>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
+        else f3_rows<KR, true, false>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
+      }
       __syncwarp();
       continue;
     }
@@ -478,7 +507,8 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
       f3_stage<false, false>(S, nullptr, xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0)) + p0, n,
                       fma_(a1, (float)p0, a0), a1, lxy, lane);
       __syncwarp();
-      f3_rows<KR, true>(acc, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
+      if (ov) f3_rows<KR, true, true>(acc, ovw, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
+      else f3_rows<KR, true, false>(acc, ovw, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
       __syncwarp();
     }
   }
@@ -487,13 +517,18 @@ __device__ __forceinline__ void f3_process(F3Smem& S, int nent, float (&acc)[KR]
 template <int KR, bool VEC>
 __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
-    const float* __restrict__ xT, float* __restrict__ y, int accumulate, long long task0, long long ntasks) {
+    const float* __restrict__ xT, float* __restrict__ y, int accumulate, int parity, int tile_step,
+    long long task0, long long ntasks) {
   extern __shared__ __align__(16) unsigned char f3_smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   F3Smem& S = reinterpret_cast<F3Smem*>(f3_smem_raw)[warp];
   const long long task = task0 + (long long)blockIdx.x * F3_WARPS + warp;
   if (task >= ntasks) return;  // warp-uniform; no CTA barriers in this kernel
-  const int ntiles = (gp.nc + F3_CW - 1) / F3_CW;
+  // this launch's tiles: every other one (parity 0: even, 1: odd; see the
+  // stores at the end)
+  // (tile_step 1: every tile, no overhang)
+  const bool ovmode = tile_step == 2;
+  const int ntiles = ((gp.nc + F3_CW - 1) / F3_CW + tile_step - 1 - parity) / tile_step;
   // band-major task order; within a band, chunks of F3_VCH consecutive views x
   // all tiles, so the CTAs resident at once cover a few degrees of rotation
   // whose wedges stay in L2
@@ -507,7 +542,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
   const int tile = rem / cv;
   const int vb = vch * F3_VCH + rem % cv;
   const int v = vb % gp.nv, b = vb / gp.nv;
-  const int c0 = tile * F3_CW;
+  const int c0 = (tile_step * tile + parity) * F3_CW;
   const int cw = min(F3_CW, gp.nc - c0);
   const int rw0 = band * 32 * KR;
   const int nrows = min(32 * KR, gp.nr - rw0);
@@ -537,10 +572,11 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
   const float* xb = xT + (size_t)b * ((size_t)gp.nx * gp.ny) * gp.nz;
   // front pads of the G / X table (never rewritten); the RAW staging reads
   // the cp.async buffers past nst: keep them finite
-  for (int i = lane; i < F3_PAD; i += 32) {
-    S.G[i] = 0.0f;
-    S.X[i] = 0.0f;
-  }
+  for (int i = lane; i < F3_PAD; i += 32) S.G[i] = 0.0f;
+  float2* ovw = ovmode ? reinterpret_cast<float2*>(f3_smem_raw + sizeof(F3Smem) * F3_WARPS) + 32 * KR * warp
+                      : nullptr;
+  if (ovmode)
+    for (int i = lane; i < 32 * KR; i += 32) ovw[i] = make_float2(0.0f, 0.0f);
   if (VEC)
     for (int i = lane; i < F3_XCAP; i += 32) S.xr[i] = 0.0f;
   __syncwarp();
@@ -572,37 +608,54 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
       pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
-                               primary_x, c0, cw, rw0, nrows, VEC, g_adj);
+                               primary_x, c0, cw, rw0, nrows, VEC, ovmode, g_adj);
       __syncwarp();
       if (pending >= 16) {
-        f3_process<KR, VEC>(S, pending, acc, xb, lane);
+        f3_process<KR, VEC>(S, ovw, pending, acc, xb, lane);
         pending = 0;
         __syncwarp();
       }
     }
   }
-  if (pending > 0) f3_process<KR, VEC>(S, pending, acc, xb, lane);
+  if (pending > 0) f3_process<KR, VEC>(S, ovw, pending, acc, xb, lane);
 
-  // store the tile: y[b][v][r][c0 + c], rows rw0 + 64 (k / 2) + 2 lane + k % 2
+  // store the tile: y[b][v][r][c0 + c], rows rw0 + 64 (k / 2) + 2 lane + k % 2.
+  // Launch order makes the overhang merge deterministic without atomics:
+  // parity 0 (even tiles) stores its own columns and its overhang into the
+  // next (odd) tile's first two columns; parity 1 then adds its own first
+  // two columns onto those, stores its last two, and adds its overhang onto
+  // the next (even) tile's first two.  With `accumulate` every store adds.
+  __syncwarp();
   float* yv = y + ((size_t)b * gp.nv + v) * (size_t)gp.nr * gp.nc;
-  const bool v4 = cw == F3_CW && (gp.nc & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+  const bool v2 = (gp.nc & 1) == 0 && (reinterpret_cast<uintptr_t>(y) & 7) == 0;
+  const bool ovc = ovmode && c0 + F3_CW < gp.nc;  // the next tile exists
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
     const int r = 64 * (k >> 1) + 2 * lane + (k & 1);
     if (r >= nrows) continue;
     float* row = yv + (size_t)(rw0 + r) * gp.nc + c0;
-    if (v4) {
-      float4 o = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
-      if (accumulate) {
-        const float4 p = *reinterpret_cast<const float4*>(row);
-        o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+    const float2 o = ovc ? ovw[r] : make_float2(0.0f, 0.0f);
+    if (v2 && cw == F3_CW) {
+      float2 lo = make_float2(acc[k][0], acc[k][1]), hi = make_float2(acc[k][2], acc[k][3]);
+      if (accumulate || parity) lo = add2_(lo, *reinterpret_cast<const float2*>(row));
+      if (accumulate) hi = add2_(hi, *reinterpret_cast<const float2*>(row + 2));
+      *reinterpret_cast<float2*>(row) = lo;
+      *reinterpret_cast<float2*>(row + 2) = hi;
+      if (ovc) {
+        float2 n2 = o;
+        if (accumulate || parity) n2 = add2_(n2, *reinterpret_cast<const float2*>(row + 4));
+        *reinterpret_cast<float2*>(row + 4) = n2;
       }
-      *reinterpret_cast<float4*>(row) = o;
     } else {
 #pragma unroll
       for (int c = 0; c < F3_CW; ++c) {
         if (c >= cw) break;
-        row[c] = accumulate ? row[c] + acc[k][c] : acc[k][c];
+        row[c] = (accumulate || (parity && c < F3_OV)) ? row[c] + acc[k][c] : acc[k][c];
+      }
+      if (ovc) {
+        const int no = min(F3_OV, gp.nc - c0 - F3_CW);
+        if (no > 0) row[F3_CW] = (accumulate || parity) ? row[F3_CW] + o.x : o.x;
+        if (no > 1) row[F3_CW + 1] = (accumulate || parity) ? row[F3_CW + 1] + o.y : o.y;
       }
     }
   }
@@ -611,7 +664,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
 template <int KR>
 static cudaError_t launch_forward3d(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
                                    float* sino, int batch, bool accumulate, cudaStream_t st) {
-  const size_t smem = sizeof(F3Smem) * F3_WARPS;
+  const size_t smem = sizeof(F3Smem) * F3_WARPS + sizeof(float2) * 32 * KR * F3_WARPS;
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
   if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
@@ -619,16 +672,23 @@ static cudaError_t launch_forward3d(const GridParams& gp, const ViewCoef* vcoef,
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long nbands = (gp.nr + 32 * KR - 1) / (32 * KR);
-  const long long ntiles = (gp.nc + F3_CW - 1) / F3_CW;
-  const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
+  const long long ntiles_all = (gp.nc + F3_CW - 1) / F3_CW;
   const long long max_blocks = 1LL << 30;
   GridParams g2 = gp;
   g2.batch = batch;  // the task decode needs the batch extent
-  for (long long t0 = 0; t0 < ntasks; t0 += max_blocks * F3_WARPS) {
-    const long long rem = ntasks - t0;
-    const long long nb = (rem + F3_WARPS - 1) / F3_WARPS;
-    const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
-    kern<<<grid, F3_WARPS * 32, smem, st>>>(g2, vcoef, vax, xT, sino, accumulate ? 1 : 0, t0, ntasks);
+  // even tiles, then odd tiles (the overhang merge, see the kernel's stores)
+  static const int step_env = getenv("CTP_F3_STEP") ? atoi(getenv("CTP_F3_STEP")) : 2;  // (A/B: 1 = no overhang)
+  const int step = step_env == 1 ? 1 : 2;
+  for (int parity = 0; parity < step; ++parity) {
+    const long long ntiles = (ntiles_all + step - 1 - parity) / step;
+    const long long ntasks = nbands * ntiles * (long long)gp.nv * batch;
+    for (long long t0 = 0; t0 < ntasks; t0 += max_blocks * F3_WARPS) {
+      const long long rem = ntasks - t0;
+      const long long nb = (rem + F3_WARPS - 1) / F3_WARPS;
+      const unsigned grid = (unsigned)(nb < max_blocks ? nb : max_blocks);
+      kern<<<grid, F3_WARPS * 32, smem, st>>>(g2, vcoef, vax, xT, sino, accumulate ? 1 : 0, parity, step, t0,
+                                              ntasks);
+    }
   }
   return cudaGetLastError();
 }
