@@ -73,12 +73,47 @@ for rep in reps:
                     stalls[k[len(STALL):]] = float(x[i].replace(",", ""))
                 except ValueError:
                     pass
+        if "nan" in x[h.index("smsp__inst_executed.sum")].lower():
+            continue  # an incomplete replay (metrics not collected): skip the launch
         cols.append((name, vals, stalls))
 
 
 def val(v, m):
     s, u = v[m]
     return float(s.replace(",", "")) * scale.get(u, 1)
+
+
+# a kernel launched more than once per projection (the forward's even / odd
+# tile launches) is one column: additive metrics summed, rates and shares
+# weighted by launch time
+ADD = {"gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
+       "smsp__inst_executed.sum", "sass__inst_executed_register_spilling",
+       "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+       "launch__grid_size"}
+merged = {}
+for name, v, st in cols:
+    if name not in merged:
+        merged[name] = ([v], [st])
+    else:
+        merged[name][0].append(v)
+        merged[name][1].append(st)
+cols = []
+for name, (vs, sts) in merged.items():
+    t = [val(v, "gpu__time_duration.sum") for v in vs]
+    out = {}
+    for w in want:
+        if not all(w in v for v in vs):
+            continue
+        nums = [val(v, w) for v in vs]
+        x = sum(nums) if w in ADD else sum(a * b for a, b in zip(nums, t)) / sum(t)
+        unit = vs[0][w][1]
+        out[w] = (repr(x / scale.get(unit, 1)), unit)
+    stt = {}
+    for st in sts:
+        for k, c in st.items():
+            stt[k] = stt.get(k, 0.0) + c
+    cols.append((name + (f" (x{len(vs)} launches)" if len(vs) > 1 else ""), out, stt))
 
 
 traffic = {}
@@ -101,6 +136,7 @@ with open(f"profiles/{tag}_ncu.md", "w") as f:
         top = sorted(st.items(), key=lambda kv: -kv[1])[:5]
         f.write(f"* `{name}`: " + ", ".join(f"{k} {100 * c / s:.1f}%" for k, c in top) + "\n")
     for name, v, st in cols:
+        name = name.split(" (x")[0]
         traffic[name] = {"dram_bytes_per_launch": (val(v, "dram__bytes_read.sum") + val(v, "dram__bytes_write.sum"))
                          * (720.0 / views),
                          "views_in_capture": views,
