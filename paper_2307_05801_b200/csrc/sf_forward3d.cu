@@ -72,10 +72,10 @@ struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
   int info;       // g0 | g1 << 5 | fast << 10 | nst << 11 (nst staged slices; 0: misses the band)
   float cu;       // u(r + 1/2) = r invB + cu: upper boundary of band row r in staged-slice units
   float invB;     // 1 / rows per slice
-  float lxy;      // amp(s) = lxy sqrt(1 + (a0 + a1 s)^2), s = staged slice index
-  float a0, a1;
+  int resv;
+  float a0, a1;   // amp(s) = lxy sqrt(1 + (a0 + a1 s)^2), s = staged slice index (lxy is in bts)
   unsigned gadj;   // the warp's G table base + F3_PAD - (bits of 1.5 * 2^23) entries (opaque; see f3_eval)
-  float bts[F3_CW + F3_OV];  // B * ts(c) of columns c0 .. c0 + 5 (own 4 + overhang 2; 0 outside)
+  float bts[F3_CW + F3_OV];  // B lxy ts(c) of columns c0 .. c0 + 5 (own 4 + overhang 2; 0 outside)
   int has_ov;      // the overhang weights are not all zero
   int pad;
 };
@@ -133,14 +133,14 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
   const double Lo = A + B * ((double)za4 - 0.5);  // lower boundary of staged slice 0
   e.cu = (float)((0.5 - Lo) * invB);
   e.invB = (float)invB;
-  e.lxy = f.lxy;
+  e.resv = 0;
   e.a1 = f.a1;
   e.a0 = fma_(f.a1, (float)za4, f.a0);
   e.gadj = 0u;
   const Trap p = make_trap(f);
   float ts[F3_CW + F3_OV];
   col_weights<F3_CW + F3_OV>(p, c0, ts);
-  const float Bf = (float)B;
+  const float Bf = (float)B * f.lxy;  // the amplitude's constant factor, out of the staging
   bool ov = false;
 #pragma unroll
   for (int c = 0; c < F3_CW + F3_OV; ++c) {
@@ -211,7 +211,7 @@ __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* 
 //   Otherwise (global x): slices >= n read as 0 and X[n] = 0.
 template <bool RAW, bool VEC>
 __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const float* __restrict__ xg, int n, float a0,
-                                         float a1, float lxy, int lane) {
+                                         float a1, int lane) {
   float carry = 0.0f;
 #pragma unroll
   for (int c = 0; c < F3_XCAP / 256; ++c) {
@@ -242,8 +242,8 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
       const float2 iA = make_float2(sf, sf + 1.0f), iB = make_float2(sf + 2.0f, sf + 3.0f);
       const float2 qA = fma2_(bc2_(a1), iA, bc2_(a0)), qB = fma2_(bc2_(a1), iB, bc2_(a0));
       const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
-      const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
-      const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
+      const float2 ampA = make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y));
+      const float2 ampB = make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y));
       xa[2 * h] = mul2_(ampA, make_float2(v.x, v.y));
       xa[2 * h + 1] = mul2_(ampB, make_float2(v.z, v.w));
     }
@@ -281,43 +281,50 @@ __device__ __forceinline__ void f3_stage(F3Smem& S, const float* xraw, const flo
   for (int i = lane; i <= F3_PAD + 1; i += 32) S.G[F3_PAD + n + i] = total;  // (G_n+1 too: lerp)
 }
 
-// RAW staging of up to F3_XCAP slices with both 256-slice chunks in flight:
-// the four 128-slice groups' loads, amplitudes, local prefixes and warp
-// scans are independent (only the final offsets chain), so their latency
-// chains interleave.  Same layout and results as f3_stage<true, *>.
-__device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, int n, float a0, float a1, float lxy,
+// Inclusive warp scans of four series at once, step d: the predicated adds
+// update the sums in place (no select / copy per series).
+__device__ __forceinline__ void f3_scan_step4(float (&v)[4], int d) {
+  asm("{.reg .pred p;\n\t.reg .f32 t0, t1, t2, t3;\n\t"
+      "shfl.sync.up.b32 t0|p, %0, %4, 0, -1;\n\t"
+      "shfl.sync.up.b32 t1, %1, %4, 0, -1;\n\t"
+      "shfl.sync.up.b32 t2, %2, %4, 0, -1;\n\t"
+      "shfl.sync.up.b32 t3, %3, %4, 0, -1;\n\t"
+      "@p add.f32 %0, %0, t0;\n\t@p add.f32 %1, %1, t1;\n\t"
+      "@p add.f32 %2, %2, t2;\n\t@p add.f32 %3, %3, t3;}"
+      : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]) : "r"(d));
+}
+
+// RAW staging of F3_XCAP slices from the cp.async buffer, whose slices past
+// the column's n are zero-filled by the copy (so G[k] = G[n], the total, for
+// n <= k <= F3_XCAP without a fix-up), with the four 128-slice groups in
+// flight: lane t owns slices 128 q + 4 t .. + 3 of group q; amp * x, local
+// prefixes, four warp scans (only the final offsets chain).  The back pad
+// past F3_XCAP holds the total.  Same values as f3_stage<true, *> for k <= n.
+__device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, float a0, float a1, float lanef4,
                                              int lane) {
   static_assert(F3_XCAP == 512, "four groups of 128 slices");
-  float2 xa[4][2];
-  float t[4], inc[4], p1[4], p2[4], p3[4];
+  static_assert((F3_PAD + 4) % 4 == 0 && (F3_PAD + 4) / 4 <= 64, "back pad: two float4 rounds");
+  float p1[4], p2[4], p3[4], t[4], inc[4];
+  // the slope factor q(s) = a0 + a1 s from the lane's first slice (no
+  // per-slice index conversions)
+  const float qb = fmaf(a1, lanef4, a0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int s = 128 * q + 4 * lane;
     const float4 v = *reinterpret_cast<const float4*>(xraw + s);
-    const float sf = (float)s;
-    const float2 iA = make_float2(sf, sf + 1.0f), iB = make_float2(sf + 2.0f, sf + 3.0f);
-    const float2 qA = fma2_(bc2_(a1), iA, bc2_(a0)), qB = fma2_(bc2_(a1), iB, bc2_(a0));
+    const float2 qA = make_float2(fmaf(a1, (float)(128 * q), qb), fmaf(a1, (float)(128 * q + 1), qb));
+    const float2 qB = make_float2(fmaf(a1, (float)(128 * q + 2), qb), fmaf(a1, (float)(128 * q + 3), qb));
     const float2 tA = fma2_(qA, qA, bc2_(1.0f)), tB = fma2_(qB, qB, bc2_(1.0f));
-    const float2 ampA = mul2_(bc2_(lxy), make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)));
-    const float2 ampB = mul2_(bc2_(lxy), make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)));
-    xa[q][0] = mul2_(ampA, make_float2(v.x, v.y));
-    xa[q][1] = mul2_(ampB, make_float2(v.z, v.w));
-    p1[q] = xa[q][0].x;
-    p2[q] = p1[q] + xa[q][0].y;
-    p3[q] = p2[q] + xa[q][1].x;
-    t[q] = p3[q] + xa[q][1].y;
+    const float2 xa0 = mul2_(make_float2(sqrt_approx(tA.x), sqrt_approx(tA.y)), make_float2(v.x, v.y));
+    const float2 xa1 = mul2_(make_float2(sqrt_approx(tB.x), sqrt_approx(tB.y)), make_float2(v.z, v.w));
+    p1[q] = xa0.x;
+    p2[q] = p1[q] + xa0.y;
+    p3[q] = p2[q] + xa1.x;
+    t[q] = p3[q] + xa1.y;
     inc[q] = t[q];
   }
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    float nb[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) nb[q] = __shfl_up_sync(0xffffffffu, inc[q], d);
-    if (lane >= d) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) inc[q] += nb[q];
-    }
-  }
+  for (int d = 1; d < 32; d <<= 1) f3_scan_step4(inc, d);
   float tot[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) tot[q] = __shfl_sync(0xffffffffu, inc[q], 31);
@@ -325,17 +332,15 @@ __device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, int n
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const float e = base + (inc[q] - t[q]);
-    const float2 e01 = add2_(bc2_(e), make_float2(0.0f, p1[q])), e23 = add2_(bc2_(e), make_float2(p2[q], p3[q]));
     const int s = 128 * q + 4 * lane;
-    if (s <= n)  // the float4 that holds (or starts at) index n carries G[n]
-      *reinterpret_cast<float4*>(S.G + F3_PAD + s) = make_float4(e01.x, e01.y, e23.x, e23.y);
+    *reinterpret_cast<float4*>(S.G + F3_PAD + s) = make_float4(e, e + p1[q], e + p2[q], e + p3[q]);
     base += tot[q];
   }
-  // back pad (see f3_stage): G[n] as stored, or the total when n == 512
-  __syncwarp();
-  const float total = n >= F3_XCAP ? base : S.G[F3_PAD + n];
-  __syncwarp();
-  for (int i = lane; i <= F3_PAD + 1; i += 32) S.G[F3_PAD + n + i] = total;  // (G_n+1 too: lerp)
+  // back pad: entries F3_XCAP .. F3_XCAP + F3_PAD + 3 = the total
+  float4* bp = reinterpret_cast<float4*>(S.G + F3_PAD + F3_XCAP);
+  const float4 tt = make_float4(base, base, base, base);
+  bp[lane] = tt;
+  if (lane < (F3_PAD + 4) / 4 - 32) bp[32 + lane] = tt;
 }
 
 // Fn(u) = G_k + (u - k) X_k, k = floor(u), -2^22 < u < 2^22: floor by adding
@@ -401,8 +406,8 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], float2* __restr
   const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
   const float2 b45 = make_float2(bts[4], bts[5]);
   float4* ov4 = reinterpret_cast<float4*>(ovacc) + lane;  // rows 64 p + 2 lane, + 1 (two float2)
-#pragma unroll
   constexpr int NB = (KR / 2 + F3_BLK - 1) / F3_BLK;
+#pragma unroll
   for (int q = 0; q < NB; ++q) {  // blocks of F3_BLK pairs, straight-line inside
     if (F3_BLK * q + F3_BLK - 1 < p0 || F3_BLK * q > p1) continue;  // warp-uniform
 #pragma unroll
@@ -447,10 +452,13 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
         if (VEC) {
           const float* xc = xb + ((size_t)(unsigned)S.ent[e].col << 2);
           const int nst = info >> 11;
+          // the whole buffer: slices past nst (also inside the last
+          // float4) are zero-filled, see f3_stage_raw
 #pragma unroll
           for (int t = 0; t < F3_XCAP / 128; ++t) {
             const int s = 4 * lane + 128 * t;
-            if (s < nst) cp_async16(&S.xr[s], xc + s);
+            const int nb = min(max(nst - s, 0), 4);
+            cp_async16_zfill(&S.xr[s], xc + (nb > 0 ? s : 0), 4u * (unsigned)nb);
           }
           cp_async_commit();
         }
@@ -459,13 +467,14 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
     }
     return nent;
   };
+  const float lanef4 = (float)(4 * lane);
   int e_pf = next_fast(0);
   for (int e = 0; e < nent; ++e) {
     const F3Entry& E = S.ent[e];
     const int info = E.info;
     const int nst = info >> 11;
     if (nst == 0) continue;
-    const float cu = E.cu, invB = E.invB, lxy = E.lxy, a0 = E.a0, a1 = E.a1;
+    const float cu = E.cu, invB = E.invB, a0 = E.a0, a1 = E.a1;
     const unsigned g_adj = E.gadj;
     const int g0 = info & 31, g1 = (info >> 5) & 31;
     float bts[F3_CW + F3_OV];
@@ -480,16 +489,17 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
         __syncwarp();
         xraw = S.xr;
       }
-      if (VEC) f3_stage_raw(S, xraw, nst, a0, a1, lxy, lane);
-      else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lxy, lane);
+      if (VEC) f3_stage_raw(S, xraw, a0, a1, lanef4, lane);
+      else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
       // unclamped when every evaluated row (whole blocks around [g0, g1]) maps
       // into the padded table
       const int q0 = (g0 >> 1) / F3_BLK, q1 = (g1 >> 1) / F3_BLK;
       const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), 32 * KR) - 1;
+      // (the vector path's table holds the total up to F3_XCAP + F3_PAD + 3)
       const bool inside = fmaf((float)rlo - 1.0f, invB, cu) >= 1.0f - (float)F3_PAD &&
-                          fmaf((float)rhi, invB, cu) <= (float)(nst + F3_PAD) - 1.0f;
+                          fmaf((float)rhi, invB, cu) <= (float)((VEC ? F3_XCAP : nst) + F3_PAD) - 1.0f;
       if (inside) {
         if (ov) f3_rows<KR, false, true>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
         else f3_rows<KR, false, false>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
@@ -505,7 +515,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
     for (int p0 = 0; p0 < nst; p0 += F3_XCAP) {
       const int n = min(F3_XCAP, nst - p0);
       f3_stage<false, false>(S, nullptr, xb + ((size_t)(unsigned)E.col << (VEC ? 2 : 0)) + p0, n,
-                      fma_(a1, (float)p0, a0), a1, lxy, lane);
+                      fma_(a1, (float)p0, a0), a1, lane);
       __syncwarp();
       if (ov) f3_rows<KR, true, true>(acc, ovw, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);
       else f3_rows<KR, true, false>(acc, ovw, g_adj, cu - (float)p0, invB, bts, n, g0, g1, lane);

@@ -29,7 +29,7 @@ def main():
     if a.compare:
         p, q = np.load(a.compare[0]), np.load(a.compare[1])
         res = {}
-        for k in p.files:
+        for k in sorted(set(p.files) & set(q.files)):
             x, y = p[k].astype(np.float64), q[k].astype(np.float64)
             res[k] = dict(rel_l2=float(np.linalg.norm(x - y) / np.linalg.norm(y)),
                           max_abs_rel=float(np.abs(x - y).max() / np.abs(y).max()))
