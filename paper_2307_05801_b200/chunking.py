@@ -136,6 +136,23 @@ def plan_blocks(g, spec, batch: int, budget: int):
         f"({view_bytes} B) per block need {block_bytes(g, spec, batch, 1, 1)} B")
 
 
+def taper(ranges, direction: int, first: int = 32):
+    """Split the chunk whose transfer is exposed -- the back projection's
+    first upload (direction 1), the forward projection's last download (0) --
+    so that only ``first`` views' worth of it waits: [a, e) -> [a, a + first),
+    [a + first, e) (mirrored for the forward) when e - a >= 2 first.  The rest
+    of the split chunk moves while the small one computes (a view transfers
+    several times faster than it projects)."""
+    rs = list(ranges)
+    if len(rs) < 2:
+        return rs
+    if direction == 1:
+        a, e = rs[0]
+        return [(a, a + first), (a + first, e)] + rs[1:] if e - a >= 2 * first else rs
+    a, e = rs[-1]
+    return rs[:-1] + [(a, e - first), (e - first, e)] if e - a >= 2 * first else rs
+
+
 def _flat(buf, shape):
     """Contiguous view of the first prod(shape) elements of a flat buffer."""
     n = 1
@@ -159,6 +176,8 @@ def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = N
         nzs = nzs0 if nzs is None else nzs
         ranges = ranges0 if ranges is None else ranges
     zr = zslab_ranges(nz, min(nzs, nz))
+    if len(zr) == 1:
+        ranges = taper(ranges, direction)
     one_slab, one_chunk = len(zr) == 1, len(ranges) == 1
     plans = {}
 

@@ -47,7 +47,11 @@
 
 namespace ctp {
 
-constexpr int F3_CW = 4;              // detector columns per tile
+#ifndef CTP_F3_CW
+#define CTP_F3_CW 4
+#endif
+constexpr int F3_CW = CTP_F3_CW;      // detector columns per tile (2 or 4)
+static_assert(F3_CW == 2 || F3_CW == 4, "tile width");
 // 32-row groups per warp task (KR, a template parameter): 24 (768-row bands)
 // when every column's staged slices fit one piece (nz <= F3_XCAP), else 12
 constexpr int F3_VCH = 16;            // views per chunk of the task order
@@ -75,9 +79,9 @@ struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
   int resv;
   float a0, a1;   // amp(s) = lxy sqrt(1 + (a0 + a1 s)^2), s = staged slice index (lxy is in bts)
   unsigned gadj;   // the warp's G table base + F3_PAD - (bits of 1.5 * 2^23) entries (opaque; see f3_eval)
-  float bts[F3_CW + F3_OV];  // B lxy ts(c) of columns c0 .. c0 + 5 (own 4 + overhang 2; 0 outside)
+  float bts[F3_CW + F3_OV];  // B lxy ts(c) of columns c0 .. c0 + F3_CW + 1 (own + overhang 2; 0 outside)
   int has_ov;      // the overhang weights are not all zero
-  int pad;
+  int pad[5 - F3_CW];
 };
 static_assert(sizeof(F3Entry) == 64, "F3Entry layout");
 
@@ -403,8 +407,9 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], float2* __restr
   float rot_prev = f3_eval(g_adj, ul);
   const int src = (lane + 31) & 31;
   const bool l0 = lane == 0;
-  const float2 b01 = make_float2(bts[0], bts[1]), b23 = make_float2(bts[2], bts[3]);
-  const float2 b45 = make_float2(bts[4], bts[5]);
+  const float2 b01 = make_float2(bts[0], bts[1]);
+  const float2 b23 = F3_CW == 4 ? make_float2(bts[2], bts[3]) : make_float2(0.0f, 0.0f);
+  const float2 b45 = make_float2(bts[F3_CW], bts[F3_CW + 1]);  // overhang columns
   float4* ov4 = reinterpret_cast<float4*>(ovacc) + lane;  // rows 64 p + 2 lane, + 1 (two float2)
   constexpr int NB = (KR / 2 + F3_BLK - 1) / F3_BLK;
 #pragma unroll
@@ -424,12 +429,16 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], float2* __restr
       float2 a;
       a = fma2_(b01, bc2_(d.x), make_float2(acc[2 * p][0], acc[2 * p][1]));
       acc[2 * p][0] = a.x; acc[2 * p][1] = a.y;
-      a = fma2_(b23, bc2_(d.x), make_float2(acc[2 * p][2], acc[2 * p][3]));
-      acc[2 * p][2] = a.x; acc[2 * p][3] = a.y;
+      if (F3_CW == 4) {
+        a = fma2_(b23, bc2_(d.x), make_float2(acc[2 * p][F3_CW - 2], acc[2 * p][F3_CW - 1]));
+        acc[2 * p][F3_CW - 2] = a.x; acc[2 * p][F3_CW - 1] = a.y;
+      }
       a = fma2_(b01, bc2_(d.y), make_float2(acc[2 * p + 1][0], acc[2 * p + 1][1]));
       acc[2 * p + 1][0] = a.x; acc[2 * p + 1][1] = a.y;
-      a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][2], acc[2 * p + 1][3]));
-      acc[2 * p + 1][2] = a.x; acc[2 * p + 1][3] = a.y;
+      if (F3_CW == 4) {
+        a = fma2_(b23, bc2_(d.y), make_float2(acc[2 * p + 1][F3_CW - 2], acc[2 * p + 1][F3_CW - 1]));
+        acc[2 * p + 1][F3_CW - 2] = a.x; acc[2 * p + 1][F3_CW - 1] = a.y;
+      }
       if (OV) {  // the next tile's first two columns, accumulated in shared memory
         float4 o = ov4[32 * p];
         const float2 oa = fma2_(b45, bc2_(d.x), make_float2(o.x, o.y));
@@ -525,7 +534,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
 }
 
 template <int KR, bool VEC>
-__global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_kernel(
+__global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_forward3d_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
     const float* __restrict__ xT, float* __restrict__ y, int accumulate, int parity, int tile_step,
     long long task0, long long ntasks) {
@@ -646,15 +655,18 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR > 12 ? 3 : 4) sf_forward3d_k
     float* row = yv + (size_t)(rw0 + r) * gp.nc + c0;
     const float2 o = ovc ? ovw[r] : make_float2(0.0f, 0.0f);
     if (v2 && cw == F3_CW) {
-      float2 lo = make_float2(acc[k][0], acc[k][1]), hi = make_float2(acc[k][2], acc[k][3]);
+      float2 lo = make_float2(acc[k][0], acc[k][1]);
       if (accumulate || parity) lo = add2_(lo, *reinterpret_cast<const float2*>(row));
-      if (accumulate) hi = add2_(hi, *reinterpret_cast<const float2*>(row + 2));
       *reinterpret_cast<float2*>(row) = lo;
-      *reinterpret_cast<float2*>(row + 2) = hi;
+      if (F3_CW == 4) {
+        float2 hi = make_float2(acc[k][F3_CW - 2], acc[k][F3_CW - 1]);
+        if (accumulate) hi = add2_(hi, *reinterpret_cast<const float2*>(row + 2));
+        *reinterpret_cast<float2*>(row + 2) = hi;
+      }
       if (ovc) {
         float2 n2 = o;
-        if (accumulate || parity) n2 = add2_(n2, *reinterpret_cast<const float2*>(row + 4));
-        *reinterpret_cast<float2*>(row + 4) = n2;
+        if (accumulate || parity) n2 = add2_(n2, *reinterpret_cast<const float2*>(row + F3_CW));
+        *reinterpret_cast<float2*>(row + F3_CW) = n2;
       }
     } else {
 #pragma unroll

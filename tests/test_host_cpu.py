@@ -247,3 +247,19 @@ def test_stream_planner_respects_budget():
     assert nzs < 512  # the volume no longer fits: z-slabs
     with pytest.raises(ct.CudaRuntimeError):
         chunking.plan_blocks(g, spec, 1, 1 << 20)
+
+
+def test_taper_splits_the_exposed_chunk():
+    """chunking.taper: the back's first chunk / the forward's last chunk is
+    split so only 32 views wait on their transfer; coverage is unchanged."""
+    from paper_2307_05801_b200 import chunking
+
+    r = chunking.view_chunks(720, 768 * 768 * 4, (720 * 768 * 768 * 4 + 3) // 4)
+    back, fwd = chunking.taper(r, 1), chunking.taper(r, 0)
+    assert back[0] == (0, 32) and back[1] == (32, r[0][1]) and back[2:] == r[1:]
+    assert fwd[-1] == (r[-1][1] - 32, r[-1][1]) and fwd[:-2] == r[:-1]
+    for rs in (back, fwd):
+        assert rs[0][0] == 0 and rs[-1][1] == 720
+        assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(rs, rs[1:]))
+    assert chunking.taper([(0, 720)], 1) == [(0, 720)]          # one chunk: nothing exposed to split
+    assert chunking.taper([(0, 40), (40, 80)], 1) == [(0, 40), (40, 80)]  # too small to split
