@@ -44,9 +44,10 @@ CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
 #: at most about this many view chunks per call when everything fits: each
 #: chunk is one launch (a launch tail, a re-transposed volume, a back
 #: projection's read-modify-write of its slab) while fewer chunks expose more
-#: of the first upload / last download; measured on C3 (tools/e2e_chunks.py):
-#: 1 chunk 504 ms per fwd+back call pair, 3: 478, 5: 470, 12: 496, 23: 554
-MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "4"))
+#: of the first upload / last download; measured on C3 (tools/e2e_chunks.py,
+#: with ``taper``; median fwd + back call ms): MAX_CHUNKS 1: 476, 2: 445,
+#: 3: 441, 4: 463, 6: 470
+MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "3"))
 
 
 def _torch():
