@@ -451,8 +451,8 @@ int ctp_sf_back(const ctp_plan* plan, const float* sino, float* vol, int batch, 
     return CTP_OK;
   }
   float* yT = static_cast<float*>(workspace);
-  cudaError_t e = ctp::launch_transpose(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
-  if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram");
+  cudaError_t e = ctp::launch_back_input(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
+  if (e != cudaSuccess) return cuda_fail(e, "transpose_segscan_kernel");
   KernelTimer timer(plan, 1, s, flags);
   e = ctp::launch_back(gp, plan->d_coef, plan->d_ax, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
   timer.stop();
@@ -541,6 +541,8 @@ int ctp_sf_fbp_back(const ctp_plan* plan, const float* sino, float* vol, int bat
   float* yT = static_cast<float*>(workspace);
   cudaError_t e = ctp::launch_ramp_rows_T(sino, yT, gp.nr, gp.nc, batch * gp.nv, plan->geom.pixel_width, scale, s);
   if (e != cudaSuccess) return cuda_fail(e, "ramp_rows_T_kernel");
+  e = ctp::launch_back_input_inplace(yT, gp.nr, gp.nc, batch * gp.nv, s);
+  if (e != cudaSuccess) return cuda_fail(e, "segscan_rows_kernel");
   KernelTimer timer(plan, 1, s, flags);
   e = ctp::launch_back(gp, plan->d_coef, plan->d_ax, yT, vol, batch, (flags & CTP_FLAG_ACCUMULATE) != 0, s);
   timer.stop();

@@ -190,8 +190,8 @@ int ctp_sf_back_sharded(const ctp_plan* plan, ctp_dist* d, const float* sino, fl
   }
   // the previous call's reductions read `part` of the caller's last workspace;
   // the caller's stream already waits for them (see the end of this function)
-  cudaError_t e = ctp::launch_transpose(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
-  if (e != cudaSuccess) return cuda_fail(e, "transpose sinogram");
+  cudaError_t e = ctp::launch_back_input(sino, yT, gp.nr, gp.nc, batch * gp.nv, s);
+  if (e != cudaSuccess) return cuda_fail(e, "transpose_segscan_kernel");
   // slab rows past nz (the last owner's padding) are zero
   const int pad0 = nz - d->rank * S;  // first padded row of this rank's slab
   if (pad0 < S) {

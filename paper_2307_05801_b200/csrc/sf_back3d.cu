@@ -12,14 +12,16 @@
 // where H is the integral of the piecewise-constant row profile Q:
 // H(w) = S_k + (w - k) Q_k, k = floor(w), S_k = sum_{j<k} Q_j.  The reference
 // sums tt(r) Q(r) over the 2-3 rows a slice touches (_kernels.py:738-760);
-// here a warp builds the (S, Q) table of the rows its slices reach once per
-// view (coalesced 16-byte loads along the row-contiguous sinogram, warp
-// prefix scan) and every slice costs ONE table evaluation: lanes own slices
+// here a warp builds the running sums of Q over the rows its slices reach
+// once per view and every slice costs ONE table evaluation: lanes own slices
 // lane + 32 m, each lane evaluates H at the upper boundary of its slice and
-// takes the lower one from lane - 1 with a shuffle.  Mathematically identical
-// to the reference; in fp32 the prefix sums cost ~log2(rows) bits of the
-// per-slice difference (relative error ~1e-5 per view, well inside the 1e-4
-// bar, tests/test_gpu_parity.py).
+// takes the lower one from lane - 1 with a shuffle.  The input stage
+// (sino_prefix.cu) hands the kernel per-column prefix sums over aligned
+// 128-row segments, so a table is a weighted sum of those (coalesced 16-byte
+// loads along the row-contiguous sinogram) plus one carry per segment: no
+// warp scans.  Mathematically identical to the reference; in fp32 the prefix
+// sums cost ~log2(rows) bits of the per-slice difference (relative error
+// ~1e-5 per view, well inside the 1e-4 bar, tests/test_gpu_parity.py).
 //
 // Footprint setup is lane-parallel (lane l sets up view vb + l, as in round
 // 1): transverse trapezoid and column weights in fp32 (sf_common.cuh), axial
@@ -75,7 +77,7 @@ struct B3Entry {  // one (sub-)voxel footprint of the warp's column in one view
   int R0;         // table origin: absolute row, multiple of 4
   int n4;         // table rows / 4 (0: direct path)
   int mask;       // sub-footprints of this view (bit 1: second half of a split voxel)
-  int pad;       // S table base - 2^23 entries (shared address; see b3_eval)
+  int pad;       // table base - 1 - 2^23 entries (shared address; see b3_eval)
 };
 static_assert(sizeof(B3Entry) == 64, "B3Entry layout");
 
@@ -83,7 +85,8 @@ template <int ZPL>
 struct B3Smem {
   B3Entry ents[B3_WARPS][32];
   B3Entry split[B3_WARPS];
-  float tab[B3_WARPS][B3Cfg<ZPL>::QMAX + 4];  // S_k = sum_{j<k} Q_j of the table rows (S_nq = total)
+  // [4 + k]: I_k = sum_{j<=k} Q_j of table row k; [3] = 0 (k = -1)
+  float tab[B3_WARPS][B3Cfg<ZPL>::QMAX + 4];
 };
 
 // Footprint of one (sub-)voxel for slices izs..ize: f64 axial map at the
@@ -173,68 +176,62 @@ __device__ CTP_B3_RARE void b3_split(const GridParams& gp, const ViewCoef* __res
   *e = E;
 }
 
-// ---- table: (S_k, Q_k) of rows R0 + k, k < 4 n4 --------------------------
-// Lane t builds rows 4 (32 c + t) .. + 3 of chunk c (one 16-byte load per
-// footprint column when VEC), local prefix, warp scan of the group totals,
-// running carry across chunks.  Groups outside the detector read 0 (with
-// VEC, R0 and nr are multiples of 4, so a group is entirely in or out).
+// ---- table: I_k = sum_{j<=k} Q_j (+ a constant) of rows R0 + k, k < 4 n4 ---
+// Q(r) = sum_c ts(c) y_c(r).  The input holds, per detector column, inclusive
+// prefix sums P_c over aligned kBackSeg-row segments (sino_prefix.cu), so
+// I(r) = B(seg(r)) + J(r), J = sum_c ts(c) P_c, with a base per segment:
+// B(s + 1) = B(s) + J(last row of s), B(first) = 0 (the rows of the first
+// segment before R0 add a constant, which the differences H(w') - H(w) drop).
+// Lane t takes rows 128 h + 4 t .. + 3 of table half h; with R0 a multiple
+// of 4 every half holds the same split: lanes t < o / 4 in one segment, the
+// rest in the next (o = 128 - R0 mod 128, or 128: no split).  One shuffle per
+// half (the first part's last row), no scans.
 template <int NC, bool VEC, int QMAX>
 __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const float* __restrict__ yc, int nr,
                                                  int R0, int n4, const float* ts, int lane) {
   float carry = 0.0f;
-  const int nch = (n4 + 31) >> 5;
+  const int o4 = (((-R0) & (kBackSeg - 1)) ? ((-R0) & (kBackSeg - 1)) : kBackSeg) >> 2;
+  const int nh = (4 * n4 + 127) >> 7;
 #pragma unroll 1
-  for (int c = 0; c < nch; ++c) {
-    const int g = (c << 5) + lane;
-    const int r = R0 + 4 * g;
+  for (int h = 0; h < nh; ++h) {
+    const int k0 = 128 * h + 4 * lane;  // table index of the lane's first row
+    const int r0 = R0 + k0;
     float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (g < n4) {
-      if (VEC) {
-        if (r >= 0 && r < nr) {
+    if (VEC && r0 >= 0 && r0 + 3 < nr) {
 #pragma unroll
-          for (int k = 0; k < NC; ++k) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(yc + (size_t)k * nr + r));
-            q[0] = fmaf(ts[k], a.x, q[0]);
-            q[1] = fmaf(ts[k], a.y, q[1]);
-            q[2] = fmaf(ts[k], a.z, q[2]);
-            q[3] = fmaf(ts[k], a.w, q[3]);
-          }
-        }
-      } else {
+      for (int k = 0; k < NC; ++k) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(yc + (size_t)k * nr + r0));
+        q[0] = fmaf(ts[k], a.x, q[0]);
+        q[1] = fmaf(ts[k], a.y, q[1]);
+        q[2] = fmaf(ts[k], a.z, q[2]);
+        q[3] = fmaf(ts[k], a.w, q[3]);
+      }
+    } else {
+      // rows before the detector read 0; rows past it keep the value of the
+      // last on-detector row of their segment (0 in a segment past it)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = r + i;
-          if (rr >= 0 && rr < nr) {
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + i, rc = min(r, nr - 1);
+        if (r >= 0 && (rc & ~(kBackSeg - 1)) == (r & ~(kBackSeg - 1))) {
 #pragma unroll
-            for (int k = 0; k < NC; ++k) q[i] = fmaf(ts[k], __ldg(yc + (size_t)k * nr + rr), q[i]);
-          }
+          for (int k = 0; k < NC; ++k) q[i] = fmaf(ts[k], __ldg(yc + (size_t)k * nr + rc), q[i]);
         }
       }
     }
-    const float s1 = q[0], s2 = s1 + q[1], s3 = s2 + q[2], tot = s3 + q[3];
-    float incl = tot;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const float n = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += n;
-    }
-    const float ex = carry + (incl - tot);
-    if (g < QMAX / 4) reinterpret_cast<float4*>(tab)[g] = make_float4(ex, ex + s1, ex + s2, ex + s3);
-    carry += __shfl_sync(0xffffffffu, incl, 31);
+    const float carry2 = carry + __shfl_sync(0xffffffffu, q[3], o4 - 1);
+    const float base = lane < o4 ? carry : carry2;
+    if (k0 < QMAX) reinterpret_cast<float4*>(tab)[k0 >> 2] = make_float4(base + q[0], base + q[1], base + q[2], base + q[3]);
+    carry = carry2;
   }
-  __syncwarp();
-  if (lane == 0) tab[4 * n4] = carry;  // S at the end of the table
 }
 
-// Fast table (16-byte aligned rows, every table row on the detector): lane t
-// builds rows 256 c + 4 t .. + 3 (half 0) and 256 c + 128 + 4 t .. + 3 (half
-// 1) of chunk c, so every 16-byte load and store instruction covers 512
-// contiguous bytes (no bank conflicts, 4 wavefronts); two independent warp
-// scans per chunk.  Column pointers are per lane, chunks are unrolled and
-// addressed with immediate offsets.
+// Fast table (every table row on the detector, 16-byte aligned): one 16-byte
+// load per footprint column and half per lane (512 contiguous bytes per
+// instruction), two packed FMAs, one shuffle per half.  (Issuing the loads of
+// several halves ahead measured slower: more spills at 64 registers.)
 template <int NC, int NCH, int QMAX>
 __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const float* __restrict__ yc, int nr, int nq,
-                                              const float* ts, int lane) {
+                                              int o4, const float* ts, int lane) {
   const float* p[NC];
   float2 T[NC];
 #pragma unroll
@@ -244,52 +241,31 @@ __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const flo
   }
   float4* sp4 = reinterpret_cast<float4*>(tab + 4 * lane);
   float carry = 0.0f;
+  const bool first = lane < o4;
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    if (256 * c >= nq) break;  // warp-uniform
-    const bool ok0 = 256 * c + 4 * lane < nq, ok1 = 256 * c + 128 + 4 * lane < nq;
-    float2 q0 = make_float2(0.0f, 0.0f), q1 = q0, q2 = q0, q3 = q0;  // half 0: q0 q1, half 1: q2 q3
+  for (int h = 0; h < 2 * NCH; ++h) {
+    if (128 * h >= nq) break;  // warp-uniform
+    const bool ok = 128 * h + 4 * lane < nq;  // (rows past nq are never evaluated)
+    float2 lo = make_float2(0.0f, 0.0f), hi = lo;
+    if (ok) {
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      if (ok0) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(p[k] + 256 * c));
-        q0 = fma2_(T[k], make_float2(a.x, a.y), q0);
-        q1 = fma2_(T[k], make_float2(a.z, a.w), q1);
-      }
-      if (ok1) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(p[k] + 256 * c + 128));
-        q2 = fma2_(T[k], make_float2(b.x, b.y), q2);
-        q3 = fma2_(T[k], make_float2(b.z, b.w), q3);
+      for (int k = 0; k < NC; ++k) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p[k] + 128 * h));
+        lo = fma2_(T[k], make_float2(a.x, a.y), lo);
+        hi = fma2_(T[k], make_float2(a.z, a.w), hi);
       }
     }
-    // exclusive prefixes of the lane's two 4-row groups, two warp scans
-    const float a1 = q0.x, a2 = a1 + q0.y, a3 = a2 + q1.x, ta = a3 + q1.y;
-    const float b1 = q2.x, b2 = b1 + q2.y, b3 = b2 + q3.x, tb = b3 + q3.y;
-    float ia = ta, ib = tb;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const float na = __shfl_up_sync(0xffffffffu, ia, d);
-      const float nb = __shfl_up_sync(0xffffffffu, ib, d);
-      if (lane >= d) {
-        ia += na;
-        ib += nb;
-      }
+    // (lane o4 - 1's last row ends the first part's segment; when that lane
+    // is past nq, no later row is evaluated)
+    const float carry2 = carry + __shfl_sync(0xffffffffu, hi.y, o4 - 1);
+    if (ok) {
+      const float2 cc = bc2_(first ? carry : carry2);
+      lo = add2_(lo, cc);
+      hi = add2_(hi, cc);
+      sp4[32 * h] = make_float4(lo.x, lo.y, hi.x, hi.y);
     }
-    const float tot_a = __shfl_sync(0xffffffffu, ia, 31);
-    const float tot_b = __shfl_sync(0xffffffffu, ib, 31);
-    const float ea = carry + (ia - ta), eb = (carry + tot_a) + (ib - tb);
-    const float2 e01 = add2_(bc2_(ea), make_float2(0.0f, a1)), e23 = add2_(bc2_(ea), make_float2(a2, a3));
-    const float2 f01 = add2_(bc2_(eb), make_float2(0.0f, b1)), f23 = add2_(bc2_(eb), make_float2(b2, b3));
-    if (ok0) {  // (rows past nq are never evaluated; the arrays end at QMAX)
-      sp4[64 * c] = make_float4(e01.x, e01.y, e23.x, e23.y);
-    }
-    if (ok1) {
-      sp4[64 * c + 32] = make_float4(f01.x, f01.y, f23.x, f23.y);
-    }
-    carry += tot_a + tot_b;
+    carry = carry2;
   }
-  __syncwarp();
-  if (lane == 0) tab[nq] = carry;  // S at the end of the table
 }
 
 template <int QMAX>
@@ -297,7 +273,9 @@ __device__ __forceinline__ float b3_eval(unsigned tab_adj, float w) {
   const float tf = __fadd_rd(w, 8388608.0f);
   const float fr = w - (tf - 8388608.0f);  // both subtractions exact
   const unsigned a = (unsigned)__float_as_int(tf) * 4u + tab_adj;  // one LEA
-  float S0, S1;  // H = S_k + fr Q_k with Q_k = S_k+1 - S_k
+  // tab_adj points one entry below the table: (S0, S1) = (I_k-1, I_k), i.e.
+  // H = S_k + fr Q_k with the exclusive S_k = I_k-1 and Q_k = I_k - I_k-1
+  float S0, S1;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(S0) : "r"(a));
   asm volatile("ld.shared.f32 %0, [%1 + 4];" : "=f"(S1) : "r"(a));
   return fmaf(fr, S1 - S0, S0);
@@ -389,6 +367,12 @@ __device__ __forceinline__ void b3_slices(float2 (&acc)[ZPL / 2], const B3Entry&
   }
 }
 
+// y_c(r) from the segment prefix sums of column c (sino_prefix.cu)
+__device__ __forceinline__ float b3_row(const float* __restrict__ col, int r) {
+  const float v = __ldg(col + r);
+  return (r & (kBackSeg - 1)) ? v - __ldg(col + r - 1) : v;
+}
+
 // Direct path (wide footprints, split halves, long tables): rows r0 .. r0+K-1
 // of one slice, any footprint width, rows off the detector skipped.
 __device__ CTP_B3_RARE float b3_voxel_direct(float acc, float amp, float lo, float hi, const B3Entry& e,
@@ -403,12 +387,12 @@ __device__ CTP_B3_RARE float b3_voxel_direct(float acc, float amp, float lo, flo
     float q = 0.0f;
     if (r >= 0 && r < nr) {
       if (e.ncol <= B3_NCF) {
-        for (int c = 0; c < e.ncol; ++c) q = fma_(e.ts[c], __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+        for (int c = 0; c < e.ncol; ++c) q = fma_(e.ts[c], b3_row(yv + (size_t)(e.cl + c) * nr, r), q);
       } else {
         float prev = trap_cum(wide, sub_((float)e.cl, 0.5f));
         for (int c = 0; c < e.ncol; ++c) {
           const float cur = trap_cum(wide, add_((float)(e.cl + c), 0.5f));
-          q = fma_(sub_(cur, prev), __ldg(yv + (size_t)(e.cl + c) * nr + r), q);
+          q = fma_(sub_(cur, prev), b3_row(yv + (size_t)(e.cl + c) * nr, r), q);
           prev = cur;
         }
       }
@@ -436,9 +420,11 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
   const int nr = gp.nr;
   const size_t view_elems = (size_t)gp.nc * nr;
   const float* yb = yT + (size_t)b * gp.nv * view_elems;
-  float* tab = SM.tab[warp];
-  // table base minus 2^23 entries (b3_eval indexes it with the float bits)
-  const unsigned tab_adj = (unsigned)__cvta_generic_to_shared(tab) - 0x4B000000u * 4u;
+  float* tab = SM.tab[warp] + 4;  // row k at tab[k]; tab[-1] = 0
+  if (lane < 4) SM.tab[warp][lane] = 0.0f;
+  // table base minus one entry minus 2^23 entries (b3_eval indexes it with
+  // the float bits and reads (I_k-1, I_k))
+  const unsigned tab_adj = (unsigned)__cvta_generic_to_shared(tab) - 4u - 0x4B000000u * 4u;
   B3Entry(&my)[32] = SM.ents[warp];
   B3Entry& sp = SM.split[warp];
   const int span = ize - izs;  // this lane's slices: izs + lane + 32 m, m < nvalid
@@ -484,11 +470,13 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
         if (VEC && e.R0 >= 0 && e.R0 + 4 * e.n4 <= nr) {
           const float* yr = yc + e.R0;
           const int nq = 4 * e.n4;
+          // lanes of each half before the segment boundary (all: none inside)
+          const int o4 = (((-e.R0) & (kBackSeg - 1)) ? ((-e.R0) & (kBackSeg - 1)) : kBackSeg) >> 2;
           switch (ncol) {  // warp-uniform: load only the footprint's columns
-            case 1: b3_table_fast<1, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-            case 2: b3_table_fast<2, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-            case 3: b3_table_fast<3, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
-            default: b3_table_fast<4, NCH, Cfg::QMAX>(tab, yr, nr, nq, ts, lane); break;
+            case 1: b3_table_fast<1, NCH, Cfg::QMAX>(tab, yr, nr, nq, o4, ts, lane); break;
+            case 2: b3_table_fast<2, NCH, Cfg::QMAX>(tab, yr, nr, nq, o4, ts, lane); break;
+            case 3: b3_table_fast<3, NCH, Cfg::QMAX>(tab, yr, nr, nq, o4, ts, lane); break;
+            default: b3_table_fast<4, NCH, Cfg::QMAX>(tab, yr, nr, nq, o4, ts, lane); break;
           }
         } else {
           switch (ncol) {
@@ -564,8 +552,8 @@ cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewA
                         float* vol, int batch, bool accumulate, cudaStream_t st, int z0, int z1) {
   if (z1 < 0) z1 = gp.nz;
   if (z0 < 0 || z0 >= z1 || z1 > gp.nz) return cudaErrorInvalidValue;
-  static const bool legacy = getenv("CTP_BACK_LEGACY") != nullptr;  // A/B against round 1's kernel
-  if (legacy) return launch_back_legacy(gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
+  if (back_legacy()) return launch_back_legacy(  // A/B against round 1's kernel (raw input)
+      gp, vcoef, vax, yT, vol, batch, accumulate, st, z0, z1);
   const bool vec = gp.nr % 4 == 0 && (reinterpret_cast<uintptr_t>(yT) & 15) == 0;
   static const int zpl_env = getenv("CTP_B3_ZPL") ? atoi(getenv("CTP_B3_ZPL")) : 16;  // (tuning)
   // slices per warp: 512 (16 per lane) for tall z-ranges, 256 for the

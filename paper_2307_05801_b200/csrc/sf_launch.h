@@ -16,8 +16,16 @@ cudaError_t launch_transpose(const float* in, float* out, int R, int C, int batc
 // sino: [batch][nv][nr][nc]
 cudaError_t launch_forward(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* xT,
                            float* sino, int batch, bool accumulate, cudaStream_t st);
-// yT: sinogram in [batch][nv][nc][nr] layout; vol: [batch][nz][ny][nx]; only
-// slices [z0, z1) of vol are written (z1 < 0: nz)
+// Back projection input (sino_prefix.cu): the sinogram [nviews][nr][nc] as
+// [nviews][nc][nr] inclusive prefix sums over aligned kBackSeg-row segments
+// of each column (raw, only transposed, with CTP_BACK_LEGACY); the in-place
+// variant scans an already row-contiguous sinogram (FBP)
+constexpr int kBackSeg = 128;
+bool back_legacy();
+cudaError_t launch_back_input(const float* sino, float* yT, int nr, int nc, int nviews, cudaStream_t st);
+cudaError_t launch_back_input_inplace(float* yT, int nr, int nc, int nviews, cudaStream_t st);
+// yT: sinogram from launch_back_input, [batch][nv][nc][nr]; vol: [batch][nz][ny][nx];
+// only slices [z0, z1) of vol are written (z1 < 0: nz)
 constexpr int kBackZBlock = 256;  // slices per back-kernel z-block (BK_ZC)
 cudaError_t launch_back(const GridParams& gp, const ViewCoef* vcoef, const ViewAx* vax, const float* yT,
                         float* vol, int batch, bool accumulate, cudaStream_t st, int z0 = 0, int z1 = -1);
