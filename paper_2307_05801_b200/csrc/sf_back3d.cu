@@ -204,14 +204,23 @@ __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const 
     const int k0 = 128 * h + 4 * lane;  // table index of the lane's first row
     const int r0 = R0 + k0;
     float q[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (VEC && r0 >= 0 && r0 + 3 < nr) {
+    if (VEC) {
+      // nr and R0 multiples of 4: a 4-row group is entirely on or off the
+      // detector; a group past it in the last row's segment takes that row
+      if (r0 >= 0 && r0 < nr) {
 #pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(yc + (size_t)k * nr + r0));
-        q[0] = fmaf(ts[k], a.x, q[0]);
-        q[1] = fmaf(ts[k], a.y, q[1]);
-        q[2] = fmaf(ts[k], a.z, q[2]);
-        q[3] = fmaf(ts[k], a.w, q[3]);
+        for (int k = 0; k < NC; ++k) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(yc + (size_t)k * nr + r0));
+          q[0] = fmaf(ts[k], a.x, q[0]);
+          q[1] = fmaf(ts[k], a.y, q[1]);
+          q[2] = fmaf(ts[k], a.z, q[2]);
+          q[3] = fmaf(ts[k], a.w, q[3]);
+        }
+      } else if (r0 >= nr && ((nr - 1) & ~(kBackSeg - 1)) == (r0 & ~(kBackSeg - 1))) {
+        float v = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) v = fmaf(ts[k], __ldg(yc + (size_t)k * nr + nr - 1), v);
+        q[0] = q[1] = q[2] = q[3] = v;
       }
     } else {
       // rows before the detector read 0; rows past it keep the value of the

@@ -73,9 +73,10 @@ for rep in reps:
                     stalls[k[len(STALL):]] = float(x[i].replace(",", ""))
                 except ValueError:
                     pass
-        if "nan" in x[h.index("smsp__inst_executed.sum")].lower():
-            continue  # an incomplete replay (metrics not collected): skip the launch
-        cols.append((name, vals, stalls))
+        partial = "nan" in x[h.index("smsp__inst_executed.sum")].lower()
+        # an incomplete replay (metrics not collected) keeps only its duration:
+        # the kernel's complete launches stand in for it, scaled by time
+        cols.append((name, vals, stalls, partial))
 
 
 def val(v, m):
@@ -92,28 +93,38 @@ ADD = {"gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
        "launch__grid_size"}
 merged = {}
-for name, v, st in cols:
-    if name not in merged:
-        merged[name] = ([v], [st])
+for name, v, st, partial in cols:
+    merged.setdefault(name, ([], [], []))
+    if partial:
+        merged[name][2].append(val(v, "gpu__time_duration.sum"))
     else:
         merged[name][0].append(v)
         merged[name][1].append(st)
 cols = []
-for name, (vs, sts) in merged.items():
+for name, (vs, sts, tpart) in merged.items():
+    if not vs:
+        continue
     t = [val(v, "gpu__time_duration.sum") for v in vs]
+    grow = (sum(t) + sum(tpart)) / sum(t)  # incomplete launches, by time
     out = {}
     for w in want:
         if not all(w in v for v in vs):
             continue
         nums = [val(v, w) for v in vs]
-        x = sum(nums) if w in ADD else sum(a * b for a, b in zip(nums, t)) / sum(t)
+        x = sum(nums) * grow if w in ADD else sum(a * b for a, b in zip(nums, t)) / sum(t)
+        if w == "launch__grid_size":
+            x = sum(nums) * (len(vs) + len(tpart)) / len(vs)
         unit = vs[0][w][1]
         out[w] = (repr(x / scale.get(unit, 1)), unit)
     stt = {}
     for st in sts:
         for k, c in st.items():
             stt[k] = stt.get(k, 0.0) + c
-    cols.append((name + (f" (x{len(vs)} launches)" if len(vs) > 1 else ""), out, stt))
+    n = len(vs) + len(tpart)
+    note = ""
+    if n > 1:
+        note = f" (x{n} launches" + (f"; {len(tpart)} incomplete replay(s) scaled in by time" if tpart else "") + ")"
+    cols.append((name + note, out, stt))
 
 
 traffic = {}
