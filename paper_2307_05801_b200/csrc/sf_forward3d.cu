@@ -133,7 +133,9 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
   zb = min(zb, gp.nz - 1);
   if (za > zb) return false;
   const int za4 = vec ? (za & ~3) : za;
-  const int nst = zb - za4 + 1;
+  // (vector path: whole float4s -- nz and za4 are multiples of 4, so this
+  // stays inside the column; the slices past zb reach no band row, see zb)
+  const int nst = vec ? ((zb - za4 + 4) & ~3) : zb - za4 + 1;
   const double Lo = A + B * ((double)za4 - 0.5);  // lower boundary of staged slice 0
   e.cu = (float)((0.5 - Lo) * invB);
   e.invB = (float)invB;
@@ -461,13 +463,13 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
         if (VEC) {
           const float* xc = xb + ((size_t)(unsigned)S.ent[e].col << 2);
           const int nst = info >> 11;
-          // the whole buffer: slices past nst (also inside the last
-          // float4) are zero-filled, see f3_stage_raw
+          // the whole buffer: float4s past nst (a multiple of 4 here) are
+          // zero-filled, see f3_stage_raw
+          const float* xl = xc + 4 * lane;
 #pragma unroll
           for (int t = 0; t < F3_XCAP / 128; ++t) {
-            const int s = 4 * lane + 128 * t;
-            const int nb = min(max(nst - s, 0), 4);
-            cp_async16_zfill(&S.xr[s], xc + (nb > 0 ? s : 0), 4u * (unsigned)nb);
+            const bool in = 4 * lane + 128 * t < nst;
+            cp_async16_zfill(&S.xr[4 * lane + 128 * t], xl + (in ? 128 * t : 0), in ? 16u : 0u);
           }
           cp_async_commit();
         }
