@@ -73,7 +73,7 @@ constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
 
 struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
   int col;        // x offset of the first staged slice za4 (float4 units on the vector path)
-  int info;       // g0 | g1 << 5 | fast << 10 | nst << 11 (nst staged slices; 0: misses the band)
+  int info;       // g0 | g1 << 5 | fast << 10 | inside << 11 | nst << 12 (nst staged slices; 0: misses the band)
   float cu;       // u(r + 1/2) = r invB + cu: upper boundary of band row r in staged-slice units
   float invB;     // 1 / rows per slice
   int resv;
@@ -109,7 +109,8 @@ __device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
 // (sub-)voxel centre.  Returns false if the (sub-)voxel misses the tile or
 // the band.
 __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const GridParams& gp, int col, int c0, int cw,
-                                        const ViewAx& ax, float2 cxy, int rw0, int nrows, bool vec, bool ovmode) {
+                                        const ViewAx& ax, float2 cxy, int rw0, int nrows, int band_rows, bool vec,
+                                        bool ovmode) {
   // ovmode: a footprint of at most three columns belongs to the tile of its
   // first column (the columns past the tile are its overhang, merged into the
   // next tile's outputs); a wider one is taken by every tile it touches, own
@@ -162,7 +163,14 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
   e.col = (int)xo;
   const int g0 = r_lo >> 5, g1 = r_hi >> 5;
   const bool fast = nst <= F3_XCAP;
-  e.info = g0 | (g1 << 5) | (fast ? (1 << 10) : 0) | (nst << 11);
+  // inside: every row the gather evaluates (whole blocks of F3_BLK pairs
+  // around [g0, g1]) maps into the padded table, so no clamps (f3_rows)
+  const int q0 = (g0 >> 1) / F3_BLK, q1 = (g1 >> 1) / F3_BLK;
+  const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), band_rows) - 1;
+  // (the vector path's table holds the total up to F3_XCAP + F3_PAD + 3)
+  const bool inside = fmaf((float)rlo - 1.0f, e.invB, e.cu) >= 1.0f - (float)F3_PAD &&
+                      fmaf((float)rhi, e.invB, e.cu) <= (float)((vec ? F3_XCAP : nst) + F3_PAD) - 1.0f;
+  e.info = g0 | (g1 << 5) | (fast ? (1 << 10) : 0) | (inside ? (1 << 11) : 0) | (nst << 12);
   return true;
 }
 
@@ -174,7 +182,7 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
 __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp,
                                           const ViewAx* __restrict__ vaxp, F3Entry* ent, int k, int total, int ib,
                                           int excl, int jl, bool primary_x, int c0, int cw, int rw0, int nrows,
-                                          bool vec, bool ovmode, unsigned gadj) {
+                                          int band_rows, bool vec, bool ovmode, unsigned gadj) {
   const int lane = threadIdx.x & 31;
   int o = 0;
 #pragma unroll
@@ -195,8 +203,8 @@ __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* 
     SubFoot f0, f1;
     float2 cxy0, cxy1;
     const int m = column_subs(vc, gp, ix, iy, f0, f1, cxy0, cxy1) & 3;
-    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, vec, ovmode)) mask |= 1;
-    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, vec, ovmode)) mask |= 2;
+    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, band_rows, vec, ovmode)) mask |= 1;
+    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, band_rows, vec, ovmode)) mask |= 2;
   }
   const int n = __popc(mask);
   const int ni = warp_incl_scan(n, lane);
@@ -462,7 +470,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
       if (info & (1 << 10)) {
         if (VEC) {
           const float* xc = xb + ((size_t)(unsigned)S.ent[e].col << 2);
-          const int nst = info >> 11;
+          const int nst = info >> 12;
           // the whole buffer: float4s past nst (a multiple of 4 here) are
           // zero-filled, see f3_stage_raw
           const float* xl = xc + 4 * lane;
@@ -483,7 +491,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
   for (int e = 0; e < nent; ++e) {
     const F3Entry& E = S.ent[e];
     const int info = E.info;
-    const int nst = info >> 11;
+    const int nst = info >> 12;
     if (nst == 0) continue;
     const float cu = E.cu, invB = E.invB, a0 = E.a0, a1 = E.a1;
     const unsigned g_adj = E.gadj;
@@ -504,14 +512,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
       else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
-      // unclamped when every evaluated row (whole blocks around [g0, g1]) maps
-      // into the padded table
-      const int q0 = (g0 >> 1) / F3_BLK, q1 = (g1 >> 1) / F3_BLK;
-      const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), 32 * KR) - 1;
-      // (the vector path's table holds the total up to F3_XCAP + F3_PAD + 3)
-      const bool inside = fmaf((float)rlo - 1.0f, invB, cu) >= 1.0f - (float)F3_PAD &&
-                          fmaf((float)rhi, invB, cu) <= (float)((VEC ? F3_XCAP : nst) + F3_PAD) - 1.0f;
-      if (inside) {
+      if (info & (1 << 11)) {  // unclamped (see f3_fill)
         if (ov) f3_rows<KR, false, true>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
         else f3_rows<KR, false, false>(acc, ovw, g_adj, cu, invB, bts, nst, g0, g1, lane);
       } else {
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_for
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
       pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
-                               primary_x, c0, cw, rw0, nrows, VEC, ovmode, g_adj);
+                               primary_x, c0, cw, rw0, nrows, 32 * KR, VEC, ovmode, g_adj);
       __syncwarp();
       if (pending >= 16) {
         f3_process<KR, VEC>(S, ovw, pending, acc, xb, lane);
@@ -692,6 +693,7 @@ static cudaError_t launch_forward3d(const GridParams& gp, const ViewCoef* vcoef,
   // 16-byte x loads need every voxel column (nz floats) 16-byte aligned
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
   if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
+  if (gp.nz >= (1 << 19)) return cudaErrorInvalidValue;  // staged slice counts: 19 bits of F3Entry::info
   auto kern = vec ? sf_forward3d_kernel<KR, true> : sf_forward3d_kernel<KR, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
