@@ -47,6 +47,13 @@
 #ifndef CTP_B3_TX
 #define CTP_B3_TX 0
 #endif
+// L1 prefetch of the table rows (no registers, no scoreboard): 0: none, 1:
+// every half of the view at the start of its table build (one L2 round trip
+// per view instead of one per 128-row half), 2: the next view's halves
+// before the current view's slices
+#ifndef CTP_B3_PF
+#define CTP_B3_PF 1
+#endif
 #ifndef CTP_B3_MINB
 #define CTP_B3_MINB 2  // 64 registers: 32 resident warps per SM (measured best of 8/16 warps x 2-5 CTAs)
 #endif
@@ -245,6 +252,23 @@ __device__ __forceinline__ void b3_table_generic(float* __restrict__ tab, const 
 // load per footprint column and half per lane (512 contiguous bytes per
 // instruction), two packed FMAs, one shuffle per half.  (Issuing the loads of
 // several halves ahead measured slower: more spills at 64 registers.)
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// L1 prefetch of the rows b3_table_fast reads (nq rows of NC columns from yr)
+template <int NC, int NCH>
+__device__ __forceinline__ void b3_prefetch_rows(const float* __restrict__ yr, int nr, int nq, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2 * NCH; ++h) {
+    if (128 * h >= nq) break;  // warp-uniform
+    if (128 * h + 4 * lane < nq) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) prefetch_l1(yr + k * nr + 128 * h + 4 * lane);
+    }
+  }
+}
+
 template <int NC, int NCH, int QMAX>
 __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const float* __restrict__ yc, int nr, int nq,
                                               int o4, const float* ts, int lane) {
@@ -258,6 +282,7 @@ __device__ __forceinline__ void b3_table_fast(float* __restrict__ tab, const flo
   float4* sp4 = reinterpret_cast<float4*>(tab + 4 * lane);
   float carry = 0.0f;
   const bool first = lane < o4;
+  if (CTP_B3_PF == 1) b3_prefetch_rows<NC, NCH>(yc, nr, nq, lane);
 #pragma unroll
   for (int h = 0; h < 2 * NCH; ++h) {
     if (128 * h >= nq) break;  // warp-uniform
@@ -511,6 +536,19 @@ __global__ void __launch_bounds__(B3_WARPS * 32, CTP_B3_MINB) sf_back3d_kernel(
           }
         }
         __syncwarp();
+        if (CTP_B3_PF == 2 && j + 1 < nvb) {  // the next view's rows into L1
+          const B3Entry& en = my[j + 1];
+          if (en.ncol > 0 && en.n4 > 0 && en.R0 >= 0 && en.R0 + 4 * en.n4 <= nr) {
+            constexpr int NCH = (Cfg::QMAX + 255) / 256;
+            const float* yr = yview + view_elems + (size_t)en.cl * nr + en.R0;
+            switch (en.ncol) {
+              case 1: b3_prefetch_rows<1, NCH>(yr, nr, 4 * en.n4, lane); break;
+              case 2: b3_prefetch_rows<2, NCH>(yr, nr, 4 * en.n4, lane); break;
+              case 3: b3_prefetch_rows<3, NCH>(yr, nr, 4 * en.n4, lane); break;
+              default: b3_prefetch_rows<4, NCH>(yr, nr, 4 * en.n4, lane); break;
+            }
+          }
+        }
         b3_slices<ZPL, FULL>(acc, e, lane, nvalid);
         __syncwarp();
       } else if (ncol > 0) {
