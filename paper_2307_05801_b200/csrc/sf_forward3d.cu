@@ -110,7 +110,7 @@ __device__ __forceinline__ float2 sub2f_(float2 a, float2 b) {
 // the band.
 __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const GridParams& gp, int col, int c0, int cw,
                                         const ViewAx& ax, float2 cxy, int rw0, int nrows, int band_rows, bool vec,
-                                        bool ovmode) {
+                                        bool ovmode, int ng) {
   // ovmode: a footprint of at most three columns belongs to the tile of its
   // first column (the columns past the tile are its overhang, merged into the
   // next tile's outputs); a wider one is taken by every tile it touches, own
@@ -167,9 +167,9 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
   // around [g0, g1]) maps into the padded table, so no clamps (f3_rows)
   const int q0 = (g0 >> 1) / F3_BLK, q1 = (g1 >> 1) / F3_BLK;
   const int rlo = 64 * F3_BLK * q0, rhi = min(64 * F3_BLK * (q1 + 1), band_rows) - 1;
-  // (the vector path's table holds the total up to F3_XCAP + F3_PAD + 3)
+  // (the vector path's table holds the total up to 128 ng + F3_PAD + 3)
   const bool inside = fmaf((float)rlo - 1.0f, e.invB, e.cu) >= 1.0f - (float)F3_PAD &&
-                      fmaf((float)rhi, e.invB, e.cu) <= (float)((vec ? F3_XCAP : nst) + F3_PAD) - 1.0f;
+                      fmaf((float)rhi, e.invB, e.cu) <= (float)((vec ? 128 * ng : nst) + F3_PAD) - 1.0f;
   e.info = g0 | (g1 << 5) | (fast ? (1 << 10) : 0) | (inside ? (1 << 11) : 0) | (nst << 12);
   return true;
 }
@@ -182,7 +182,7 @@ __device__ __forceinline__ bool f3_fill(F3Entry& e, const SubFoot& f, const Grid
 __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* __restrict__ vcp,
                                           const ViewAx* __restrict__ vaxp, F3Entry* ent, int k, int total, int ib,
                                           int excl, int jl, bool primary_x, int c0, int cw, int rw0, int nrows,
-                                          int band_rows, bool vec, bool ovmode, unsigned gadj) {
+                                          int band_rows, bool vec, bool ovmode, int ng, unsigned gadj) {
   const int lane = threadIdx.x & 31;
   int o = 0;
 #pragma unroll
@@ -203,8 +203,8 @@ __device__ __noinline__ int f3_candidates(const GridParams& gp, const ViewCoef* 
     SubFoot f0, f1;
     float2 cxy0, cxy1;
     const int m = column_subs(vc, gp, ix, iy, f0, f1, cxy0, cxy1) & 3;
-    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, band_rows, vec, ovmode)) mask |= 1;
-    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, band_rows, vec, ovmode)) mask |= 2;
+    if ((m & 1) && f3_fill(e0, f0, gp, col, c0, cw, ax, cxy0, rw0, nrows, band_rows, vec, ovmode, ng)) mask |= 1;
+    if ((m & 2) && f3_fill(e1, f1, gp, col, c0, cw, ax, cxy1, rw0, nrows, band_rows, vec, ovmode, ng)) mask |= 2;
   }
   const int n = __popc(mask);
   const int ni = warp_incl_scan(n, lane);
@@ -308,22 +308,24 @@ __device__ __forceinline__ void f3_scan_step4(float (&v)[4], int d) {
       : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]) : "r"(d));
 }
 
-// RAW staging of F3_XCAP slices from the cp.async buffer, whose slices past
+// RAW staging of 128 NG slices (NG groups: the fewest that hold the entry's
+// staged slices; short columns stage one or two groups) from the cp.async buffer, whose slices past
 // the column's n are zero-filled by the copy (so G[k] = G[n], the total, for
 // n <= k <= F3_XCAP without a fix-up), with the four 128-slice groups in
 // flight: lane t owns slices 128 q + 4 t .. + 3 of group q; amp * x, local
 // prefixes, four warp scans (only the final offsets chain).  The back pad
 // past F3_XCAP holds the total.  Same values as f3_stage<true, *> for k <= n.
+template <int NG>
 __device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, float a0, float a1, float lanef4,
                                              int lane) {
-  static_assert(F3_XCAP == 512, "four groups of 128 slices");
+  static_assert(F3_XCAP == 512 && (NG == 1 || NG == 2 || NG == 4), "one, two or four groups of 128 slices");
   static_assert((F3_PAD + 4) % 4 == 0 && (F3_PAD + 4) / 4 <= 64, "back pad: two float4 rounds");
   float p1[4], p2[4], p3[4], t[4], inc[4];
   // the slope factor q(s) = a0 + a1 s from the lane's first slice (no
   // per-slice index conversions)
   const float qb = fmaf(a1, lanef4, a0);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NG; ++q) {
     const int s = 128 * q + 4 * lane;
     const float4 v = *reinterpret_cast<const float4*>(xraw + s);
     const float2 qA = make_float2(fmaf(a1, (float)(128 * q), qb), fmaf(a1, (float)(128 * q + 1), qb));
@@ -338,20 +340,30 @@ __device__ __forceinline__ void f3_stage_raw(F3Smem& S, const float* xraw, float
     inc[q] = t[q];
   }
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) f3_scan_step4(inc, d);
+  for (int d = 1; d < 32; d <<= 1) {
+    if (NG == 4) {
+      f3_scan_step4(inc, d);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        const float nb = __shfl_up_sync(0xffffffffu, inc[q], d);
+        if (lane >= d) inc[q] += nb;
+      }
+    }
+  }
   float tot[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) tot[q] = __shfl_sync(0xffffffffu, inc[q], 31);
+  for (int q = 0; q < NG; ++q) tot[q] = __shfl_sync(0xffffffffu, inc[q], 31);
   float base = 0.0f;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NG; ++q) {
     const float e = base + (inc[q] - t[q]);
     const int s = 128 * q + 4 * lane;
     *reinterpret_cast<float4*>(S.G + F3_PAD + s) = make_float4(e, e + p1[q], e + p2[q], e + p3[q]);
     base += tot[q];
   }
-  // back pad: entries F3_XCAP .. F3_XCAP + F3_PAD + 3 = the total
-  float4* bp = reinterpret_cast<float4*>(S.G + F3_PAD + F3_XCAP);
+  // back pad: entries 128 NG .. 128 NG + F3_PAD + 3 = the total
+  float4* bp = reinterpret_cast<float4*>(S.G + F3_PAD + 128 * NG);
   const float4 tt = make_float4(base, base, base, base);
   bp[lane] = tt;
   if (lane < (F3_PAD + 4) / 4 - 32) bp[32 + lane] = tt;
@@ -459,7 +471,7 @@ __device__ __forceinline__ void f3_rows(float (&acc)[KR][F3_CW], float2* __restr
   }
 }
 
-template <int KR, bool VEC>
+template <int KR, bool VEC, int NG>
 __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, float (&acc)[KR][F3_CW],
                                            const float* __restrict__ xb, int lane) {
   // x of the next fast entry is in flight (cp.async, 16-byte copies on the
@@ -475,7 +487,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
           // zero-filled, see f3_stage_raw
           const float* xl = xc + 4 * lane;
 #pragma unroll
-          for (int t = 0; t < F3_XCAP / 128; ++t) {
+          for (int t = 0; t < NG; ++t) {  // the groups the staging reads
             const bool in = 4 * lane + 128 * t < nst;
             cp_async16_zfill(&S.xr[4 * lane + 128 * t], xl + (in ? 128 * t : 0), in ? 16u : 0u);
           }
@@ -508,7 +520,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
         __syncwarp();
         xraw = S.xr;
       }
-      if (VEC) f3_stage_raw(S, xraw, a0, a1, lanef4, lane);
+      if (VEC) f3_stage_raw<NG>(S, xraw, a0, a1, lanef4, lane);
       else f3_stage<false, false>(S, nullptr, xg, nst, a0, a1, lane);
       __syncwarp();
       e_pf = next_fast(e + 1);  // loads for the next entry overlap this one
@@ -536,7 +548,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
   }
 }
 
-template <int KR, bool VEC>
+template <int KR, bool VEC, int NG>
 __global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_forward3d_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
     const float* __restrict__ xT, float* __restrict__ y, int accumulate, int parity, int tile_step,
@@ -630,16 +642,16 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_for
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     for (int cbase = 0; cbase < total; cbase += 32) {
       pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
-                               primary_x, c0, cw, rw0, nrows, 32 * KR, VEC, ovmode, g_adj);
+                               primary_x, c0, cw, rw0, nrows, 32 * KR, VEC, ovmode, NG, g_adj);
       __syncwarp();
       if (pending >= 16) {
-        f3_process<KR, VEC>(S, ovw, pending, acc, xb, lane);
+        f3_process<KR, VEC, NG>(S, ovw, pending, acc, xb, lane);
         pending = 0;
         __syncwarp();
       }
     }
   }
-  if (pending > 0) f3_process<KR, VEC>(S, ovw, pending, acc, xb, lane);
+  if (pending > 0) f3_process<KR, VEC, NG>(S, ovw, pending, acc, xb, lane);
 
   // store the tile: y[b][v][r][c0 + c], rows rw0 + 64 (k / 2) + 2 lane + k % 2.
   // Launch order makes the overhang merge deterministic without atomics:
@@ -694,7 +706,11 @@ static cudaError_t launch_forward3d(const GridParams& gp, const ViewCoef* vcoef,
   const bool vec = gp.nz % 4 == 0 && (reinterpret_cast<uintptr_t>(xT) & 15) == 0;
   if ((long long)gp.nx * gp.ny * gp.nz >= (vec ? (1LL << 34) : (1LL << 32))) return cudaErrorInvalidValue;
   if (gp.nz >= (1 << 19)) return cudaErrorInvalidValue;  // staged slice counts: 19 bits of F3Entry::info
-  auto kern = vec ? sf_forward3d_kernel<KR, true> : sf_forward3d_kernel<KR, false>;
+  // 128-slice groups the vector path stages: the fewest that hold a column
+  // (short columns stage one or two groups)
+  auto kern = !vec ? sf_forward3d_kernel<KR, false, 4>
+                   : (gp.nz <= 128 ? sf_forward3d_kernel<KR, true, 1>
+                                   : (gp.nz <= 256 ? sf_forward3d_kernel<KR, true, 2> : sf_forward3d_kernel<KR, true, 4>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long nbands = (gp.nr + 32 * KR - 1) / (32 * KR);
