@@ -65,7 +65,7 @@ def run_batched(g: Geometry, spec: VolumeSpec, batch, direction: int, out=None, 
     as_numpy = not isinstance(batch, torch.Tensor)
     host = torch.from_numpy(np.ascontiguousarray(batch, dtype=np.float32)) if as_numpy else batch
     host = host.to(torch.float32).contiguous()
-    nzs, ranges = plan_blocks(g, spec, int(host.shape[0]), device_budget(plan.device))
+    nzs, ranges = plan_blocks(g, spec, int(host.shape[0]), device_budget(plan.device), direction)
     res = stream_apply(plan, host, direction, nzs, ranges)
     return res.numpy() if as_numpy else res
 

@@ -26,7 +26,9 @@ another stream).
 
 ``plan_blocks`` picks the sizes from a device budget: CTPROJ_DEVICE_BUDGET
 (bytes) if set, else 80% of the free device memory; CTPROJ_ZSLAB forces a
-slab size, CTPROJ_CHUNK_BYTES / CTPROJ_MAX_CHUNKS tune the view chunks.
+slab size, CTPROJ_CHUNK_BYTES / CTPROJ_MAX_CHUNKS (/ CTPROJ_MAX_CHUNKS_FWD for
+the forward) tune the view chunks, CTPROJ_FWD_STREAMS the forward's compute
+streams.
 Forward with one slab is bitwise identical to one resident call; slabs and
 back chunks only change the fp32 summation order (tested < 1e-6).
 """
@@ -48,6 +50,18 @@ CHUNK_BYTES = int(os.environ.get("CTPROJ_CHUNK_BYTES", str(256 << 20)))
 #: with ``taper``; median fwd + back call ms): MAX_CHUNKS 1: 476, 2: 445,
 #: 3: 441, 4: 463, 6: 470
 MAX_CHUNKS = int(os.environ.get("CTPROJ_MAX_CHUNKS", "3"))
+#: the forward's own cap: its chunks alternate on two compute streams
+#: (FWD_STREAMS), so a chunk's launch tails (~3 ms per tile-parity launch on
+#: C3: a task is one view x 4 columns x 768 rows) overlap the next chunk's
+#: start; measured on C3 (tools/e2e_ab.py, median forward call ms): 3 chunks
+#: 258.4 with one or two streams, 6 chunks 278.3 on one stream, 252.6 on two,
+#: 8 chunks 255.3 on two
+MAX_CHUNKS_FWD = int(os.environ.get("CTPROJ_MAX_CHUNKS_FWD", "6"))
+#: compute streams the forward's view chunks alternate on (volume resident)
+FWD_STREAMS = int(os.environ.get("CTPROJ_FWD_STREAMS", "2"))
+
+
+_FWD_STREAM = {}  # device index -> the forward's second compute stream
 
 
 def _torch():
@@ -102,7 +116,7 @@ def block_bytes(g, spec, batch: int, nzs: int, nvc: int) -> int:
     return 2 * xs + 2 * yc + max(xs, yc)
 
 
-def plan_blocks(g, spec, batch: int, budget: int):
+def plan_blocks(g, spec, batch: int, budget: int, direction: int = 1):
     """(nzs, view ranges) for a streamed call within ``budget`` bytes: the
     whole volume with up to MAX_CHUNKS view chunks (or 32-view chunks) when
     that fits; otherwise z-slabs with the largest view chunks that still leave
@@ -111,7 +125,7 @@ def plan_blocks(g, spec, batch: int, budget: int):
     view_bytes = 4 * batch * g.detector.numRows * g.detector.numCols
     slice_bytes = 4 * batch * spec.numX * spec.numY
     forced = int(os.environ.get("CTPROJ_ZSLAB", "0"))
-    chunk = max(CHUNK_BYTES, math.ceil(nv * view_bytes / MAX_CHUNKS))
+    chunk = max(CHUNK_BYTES, math.ceil(nv * view_bytes / (MAX_CHUNKS_FWD if direction == 0 else MAX_CHUNKS)))
     options = []
     for nvc_cap in (chunk // view_bytes, 32, 1):
         ranges = view_chunks(nv, view_bytes, max(1, nvc_cap) * view_bytes)
@@ -173,7 +187,7 @@ def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = N
     nz, ny, nx = spec.shape
     nv, nr, nc = g.shape
     if nzs is None or ranges is None:
-        nzs0, ranges0 = plan_blocks(g, spec, B, device_budget(dev))
+        nzs0, ranges0 = plan_blocks(g, spec, B, device_budget(dev), direction)
         nzs = nzs0 if nzs is None else nzs
         ranges = ranges0 if ranges is None else ranges
     zr = zslab_ranges(nz, min(nzs, nz))
@@ -218,9 +232,9 @@ def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = N
         ev.record(h2d)
         compute.wait_event(ev)
 
-    def download(out, block, sl):
+    def download(out, block, sl, after=None):
         ev = torch.cuda.Event()
-        ev.record(compute)
+        ev.record(compute if after is None else after)
         d2h.wait_event(ev)
         with torch.cuda.stream(d2h):
             dst = out if sl is None else out[:, sl[0]:sl[1]]
@@ -238,18 +252,32 @@ def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = N
             out = torch.empty((B, nv, nr, nc), dtype=torch.float32, pin_memory=True)
             yring = [torch.empty(B * nvc_max * nr * nc, dtype=torch.float32, device=dev) for _ in range(2)]
             y_free = [None, None]  # download that last read the slot
+            # with the whole volume resident, consecutive view chunks run on
+            # alternating compute streams: their outputs are disjoint and the
+            # volume is read-only, so one chunk's launch tails overlap the
+            # next chunk's start (FWD_STREAMS = 1: one stream)
+            cstreams = [compute]
             if one_slab:
                 xd = torch.empty((B, nz, ny, nx), dtype=torch.float32, device=dev)
                 upload(xd, 0, True)
+                if FWD_STREAMS > 1 and len(ranges) > 1:
+                    # one persistent stream per device: the caching allocator
+                    # keeps freed blocks per stream, so a fresh stream per call
+                    # would re-allocate the chunks' workspaces every call
+                    if dev.index not in _FWD_STREAM:
+                        _FWD_STREAM[dev.index] = torch.cuda.Stream(dev)
+                    cstreams.append(_FWD_STREAM[dev.index])
+                    cstreams[1].wait_stream(compute)
             else:
                 xring = [torch.empty(B * nzs_max * ny * nx, dtype=torch.float32, device=dev) for _ in range(2)]
                 x_free = [None, None]  # kernel that last read the slot
             step = 0
             for vi, (a, e) in enumerate(ranges):
                 k = vi % 2
+                cs = cstreams[vi % len(cstreams)]
                 ys = _flat(yring[k], (B, e - a, nr, nc))
                 if y_free[k] is not None:
-                    compute.wait_event(y_free[k])
+                    cs.wait_event(y_free[k])
                 for zi, (z0, z1) in enumerate(zr):
                     if one_slab:
                         xs = xd
@@ -259,12 +287,18 @@ def stream_apply(plan: "_native.Plan", host, direction: int, nzs: int | None = N
                             h2d.wait_event(x_free[s])
                         xs = _flat(xring[s], (B, z1 - z0, ny, nx))
                         upload(xs, zi, True)
-                    sub(zi, vi).forward(xs, out=ys, accumulate=zi > 0)
+                    if cs is compute:
+                        sub(zi, vi).forward(xs, out=ys, accumulate=zi > 0)
+                    else:
+                        with torch.cuda.stream(cs):
+                            sub(zi, vi).forward(xs, out=ys, accumulate=zi > 0)
                     if not one_slab:
                         x_free[s] = torch.cuda.Event()
                         x_free[s].record(compute)
                         step += 1
-                y_free[k] = download(out, ys, None if one_chunk else (a, e))
+                y_free[k] = download(out, ys, None if one_chunk else (a, e), after=cs)
+            for cs in cstreams[1:]:
+                compute.wait_stream(cs)
             compute.wait_stream(d2h)
             compute.synchronize()
             return out
