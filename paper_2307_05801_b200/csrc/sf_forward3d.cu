@@ -54,7 +54,14 @@ constexpr int F3_CW = CTP_F3_CW;      // detector columns per tile (2 or 4)
 static_assert(F3_CW == 2 || F3_CW == 4, "tile width");
 // 32-row groups per warp task (KR, a template parameter): 24 (768-row bands)
 // when every column's staged slices fit one piece (nz <= F3_XCAP), else 12
-constexpr int F3_VCH = 16;            // views per chunk of the task order
+#ifndef CTP_F3_VCH
+#define CTP_F3_VCH 16
+#endif
+#ifndef CTP_F3_PEND
+#define CTP_F3_PEND 8  // (measured on C3: 16: 233.9 ms, 8: 231.6, 4: 231.6, 1: 232.0)
+#endif
+constexpr int F3_VCH = CTP_F3_VCH;    // views per chunk of the task order
+constexpr int F3_PEND = CTP_F3_PEND;  // entries gathered before they are processed
 constexpr int F3_WARPS = 4;           // independent warps per CTA
 constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
 #ifndef CTP_F3_BLK
@@ -68,7 +75,7 @@ constexpr int F3_PAD = CTP_F3_PAD;    // zero slices below / total slices above 
 static_assert(F3_PAD % 4 == 0, "16-byte aligned table stores");
 constexpr int F3_TAB = F3_PAD + F3_XCAP + 4 + F3_PAD;  // G table length
 constexpr int F3_OV = 2;                               // overhang columns (the next tile's first two)
-constexpr int F3_EBUF = 80;           // >= 15 pending + 64 from one setup round
+constexpr int F3_EBUF = F3_PEND + 64;  // >= F3_PEND - 1 pending + 64 from one setup round
 
 
 struct F3Entry {  // one (sub-)voxel column reaching the task's tile and band
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_for
       pending += f3_candidates(gp, vcoef + v, vax + v, S.ent + pending, cbase + lane, total, ib, excl, jl,
                                primary_x, c0, cw, rw0, nrows, 32 * KR, VEC, ovmode, NG, g_adj);
       __syncwarp();
-      if (pending >= 16) {
+      if (pending >= F3_PEND) {
         f3_process<KR, VEC, NG>(S, ovw, pending, acc, xb, lane);
         pending = 0;
         __syncwarp();
