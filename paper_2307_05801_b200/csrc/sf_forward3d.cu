@@ -62,7 +62,10 @@ static_assert(F3_CW == 2 || F3_CW == 4, "tile width");
 #endif
 constexpr int F3_VCH = CTP_F3_VCH;    // views per chunk of the task order
 constexpr int F3_PEND = CTP_F3_PEND;  // entries gathered before they are processed
-constexpr int F3_WARPS = 4;           // independent warps per CTA
+#ifndef CTP_F3_WARPS
+#define CTP_F3_WARPS 4
+#endif
+constexpr int F3_WARPS = CTP_F3_WARPS;  // independent warps per CTA (no CTA barriers: any count)
 constexpr int F3_XCAP = 512;          // slices staged per piece (two 256-slice chunks)
 #ifndef CTP_F3_BLK
 #define CTP_F3_BLK 2
@@ -556,7 +559,7 @@ __device__ __forceinline__ void f3_process(F3Smem& S, float2* ovw, int nent, flo
 }
 
 template <int KR, bool VEC, int NG>
-__global__ void __launch_bounds__(F3_WARPS * 32, KR * F3_CW > 48 ? 3 : 4) sf_forward3d_kernel(
+__global__ void __launch_bounds__(F3_WARPS * 32, (KR * F3_CW > 48 ? 12 : 16) / F3_WARPS) sf_forward3d_kernel(
     const __grid_constant__ GridParams gp, const ViewCoef* __restrict__ vcoef, const ViewAx* __restrict__ vax,
     const float* __restrict__ xT, float* __restrict__ y, int accumulate, int parity, int tile_step,
     long long task0, long long ntasks) {
