@@ -124,7 +124,13 @@ def test_chunked_host_path(golden):
     yh = torch.from_numpy(c["y"][None].copy())
     one = chunking.host_apply(plan, xh, 0)
     many = chunking.host_apply(plan, xh, 0, chunk_bytes=16 * 16 * 4 * 3)  # 3 views per chunk
-    assert torch.equal(one, many)
+    assert torch.equal(one, many)  # (chunks alternate on two compute streams, ring slots reused)
+    streams, chunking.FWD_STREAMS = chunking.FWD_STREAMS, 1
+    try:
+        serial = chunking.host_apply(plan, xh, 0, chunk_bytes=16 * 16 * 4 * 3)
+    finally:
+        chunking.FWD_STREAMS = streams
+    assert torch.equal(serial, many)
     b1 = chunking.host_apply(plan, yh, 1)
     b3 = chunking.host_apply(plan, yh, 1, chunk_bytes=16 * 16 * 4 * 3)
     assert rel_l2(b3.numpy(), b1.numpy()) < REARRANGE_TOL
